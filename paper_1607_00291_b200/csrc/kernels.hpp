@@ -1,0 +1,35 @@
+// Device-side interface between tc_api.cpp and contract_kernels.cu.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tcb {
+
+// Tile shape of the sm_100a DMMA kernel. Tables are padded so that
+// every tile-sized table read is in bounds.
+constexpr int kBM = 128;
+constexpr int kBN = 128;
+constexpr int kBK = 16;
+constexpr int kTablePad = 128;
+
+// Launch arguments. All table pointers are device arrays of IDX (int32 or int64, per
+// `idx64`), padded with zeros; vA / vB are block-scatter flags with block size 2 over the
+// table that A / B is gathered along (1: the two entries are consecutive addresses).
+struct LaunchArgs {
+  const void* A;
+  const void* B;
+  void* C;
+  const void* rA; const void* cA; const void* rB; const void* cB; const void* rC; const void* cC;
+  const uint8_t* vA;
+  const uint8_t* vB;
+  int M, N, K;
+  double alpha, beta;
+  bool a_vec_m, b_vec_k, idx64, f32;
+};
+
+// Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
+int launch_contract(const LaunchArgs& a, cudaStream_t stream);
+
+}  // namespace tcb

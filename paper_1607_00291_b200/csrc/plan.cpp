@@ -1,0 +1,254 @@
+// Host planner for the transposition-free contraction (steps a1-a4 of DESIGN.md §Path).
+#include "plan.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+#include <numeric>
+
+namespace tcb {
+
+static int find_label(const tc_tensor& t, char x) {
+  for (int i = 0; i < t.rank; ++i)
+    if (t.labels[i] == x) return i;
+  return -1;
+}
+
+// a1 -- PAPER.md P:262-275: the labels of A and C form I, those of B and C form J, those of
+// A and B form P; a label in one tensor or in all three, or repeated within one, is rejected
+// (reading R6). Bundle order: I and P follow A's label order, J follows B's.
+Status classify(const tc_tensor& A, const tc_tensor& B, const tc_tensor& C, Bundles* out) {
+  const tc_tensor* T[3] = {&A, &B, &C};
+  for (int t = 0; t < 3; ++t) {
+    for (int i = 0; i < T[t]->rank; ++i) {
+      for (int j = 0; j < i; ++j)
+        if (T[t]->labels[i] == T[t]->labels[j])
+          return Status::err(TC_ERR_LABEL, std::string("label '") + T[t]->labels[i] +
+                                               "' repeated within one tensor");
+      char x = T[t]->labels[i];
+      int cnt = (find_label(A, x) >= 0) + (find_label(B, x) >= 0) + (find_label(C, x) >= 0);
+      if (cnt != 2)
+        return Status::err(TC_ERR_LABEL, std::string("label '") + x + "' appears in " +
+                                             std::to_string(cnt) + " tensor(s), must be 2");
+    }
+  }
+  Bundles b;
+  for (int i = 0; i < A.rank; ++i) {
+    char x = A.labels[i];
+    int ic = find_label(C, x);
+    Dim d;
+    d.len = A.lens[i];
+    d.labels = std::string(1, x);
+    if (ic >= 0) {
+      if (C.lens[ic] != d.len)
+        return Status::err(TC_ERR_SHAPE, std::string("length mismatch for '") + x + "'");
+      d.s[0] = A.strides[i];
+      d.s[1] = C.strides[ic];
+      b.I.push_back(d);
+    } else {
+      int ib = find_label(B, x);
+      if (B.lens[ib] != d.len)
+        return Status::err(TC_ERR_SHAPE, std::string("length mismatch for '") + x + "'");
+      d.s[0] = A.strides[i];
+      d.s[1] = B.strides[ib];
+      b.P.push_back(d);
+    }
+  }
+  for (int i = 0; i < B.rank; ++i) {
+    char x = B.labels[i];
+    int ic = find_label(C, x);
+    if (ic < 0) continue;
+    if (C.lens[ic] != B.lens[i])
+      return Status::err(TC_ERR_SHAPE, std::string("length mismatch for '") + x + "'");
+    Dim d;
+    d.len = B.lens[i];
+    d.labels = std::string(1, x);
+    d.s[0] = B.strides[i];
+    d.s[1] = C.strides[ic];
+    b.J.push_back(d);
+  }
+  *out = std::move(b);
+  return Status::ok();
+}
+
+// Step 2, reading R9: v folds into u when s_v = s_u * n_u in both carrying tensors;
+// pairs searched u-major over the current order, repeated until no pair folds.
+static void fold(std::vector<Dim>& dims) {
+  for (;;) {
+    bool merged = false;
+    for (size_t u = 0; u < dims.size() && !merged; ++u) {
+      for (size_t v = 0; v < dims.size(); ++v) {
+        if (u == v) continue;
+        const Dim &du = dims[u], &dv = dims[v];
+        if (dv.s[0] == du.s[0] * du.len && dv.s[1] == du.s[1] * du.len) {
+          dims[u].labels += dv.labels;
+          dims[u].len *= dv.len;
+          dims.erase(dims.begin() + (long)v);
+          merged = true;
+          break;
+        }
+      }
+    }
+    if (!merged) return;
+  }
+}
+
+static void sort_by(std::vector<Dim>& d, int which) {
+  std::stable_sort(d.begin(), d.end(), [which](const Dim& x, const Dim& y) {
+    return std::llabs(x.s[which]) < std::llabs(y.s[which]);
+  });
+}
+
+// a2 -- the five steps of P:926-934 in the paper's order (readings R9, R10).
+void normalize(Bundles* b) {
+  auto drop1 = [](std::vector<Dim>& d) {
+    d.erase(std::remove_if(d.begin(), d.end(), [](const Dim& x) { return x.len == 1; }),
+            d.end());
+  };
+  drop1(b->I); drop1(b->J); drop1(b->P);                  // 1
+  fold(b->I); fold(b->J); fold(b->P);                     // 2
+  sort_by(b->I, 1); sort_by(b->J, 1);                     // 3: C is stride slot 1 for I, J
+  b->swapped = false;
+  if (!b->J.empty() && b->J[0].s[1] == 1) {               // 4
+    std::swap(b->I, b->J);                                // I now carries (B_old, C) = (A, C)
+    for (auto& d : b->P) std::swap(d.s[0], d.s[1]);       // P: (A, B) after the swap
+    b->swapped = true;
+  }
+  sort_by(b->P, 0);                                       // 5: by stride in (new) A
+}
+
+// a3 -- scat_k = sum_d digit_d(k) * s_d, digits colexicographic.
+std::vector<int64_t> scatter(const std::vector<Dim>& dims, int which) {
+  int64_t total = 1;
+  for (const auto& d : dims) total *= d.len;
+  std::vector<int64_t> out((size_t)std::max<int64_t>(total, 0));
+  if (total <= 0) return out;
+  // incremental odometer over the dims (same values as decoding each k)
+  std::vector<int64_t> idx(dims.size(), 0);
+  int64_t off = 0;
+  for (int64_t k = 0; k < total; ++k) {
+    out[(size_t)k] = off;
+    for (size_t d = 0; d < dims.size(); ++d) {
+      if (++idx[d] < dims[d].len) { off += dims[d].s[which]; break; }
+      off -= (dims[d].len - 1) * dims[d].s[which];
+      idx[d] = 0;
+    }
+  }
+  return out;
+}
+
+// a4 -- P:678-683; a one-entry block has no difference to test and gets 1 (reading R11).
+std::vector<int64_t> block_scatter(const std::vector<int64_t>& scat, int64_t b) {
+  int64_t l = (int64_t)scat.size();
+  std::vector<int64_t> out;
+  if (b <= 0) return out;
+  for (int64_t lo = 0; lo < l; lo += b) {
+    int64_t hi = std::min(l, lo + b);
+    if (hi - lo == 1) { out.push_back(1); continue; }
+    int64_t s = scat[lo + 1] - scat[lo];
+    bool ok = s > 0;
+    for (int64_t j = lo + 1; ok && j < hi; ++j) ok = (scat[j] - scat[j - 1] == s);
+    out.push_back(ok ? s : 0);
+  }
+  return out;
+}
+
+// Reading R7: drop length <= 1 dims, sort by |stride|, each |s| must exceed the extent
+// spanned by all smaller ones.
+bool injective(int rank, const int64_t* lens, const int64_t* strides) {
+  std::vector<std::pair<int64_t, int64_t>> d;
+  for (int i = 0; i < rank; ++i) {
+    if (lens[i] == 0) return true;  // empty tensor
+    if (lens[i] > 1) d.push_back({std::llabs(strides[i]), lens[i]});
+  }
+  std::sort(d.begin(), d.end());
+  int64_t reach = 0;
+  for (auto& x : d) {
+    if (x.first < reach + 1) return false;
+    reach += x.first * (x.second - 1);
+  }
+  return true;
+}
+
+void span(int rank, const int64_t* lens, const int64_t* strides, int64_t* lo, int64_t* hi) {
+  int64_t a = 0, b = 0;
+  for (int i = 0; i < rank; ++i) {
+    if (lens[i] == 0) { *lo = 1; *hi = 0; return; }
+    int64_t e = strides[i] * (lens[i] - 1);
+    if (e < 0) a += e; else b += e;
+  }
+  *lo = a; *hi = b;
+}
+
+static int64_t max_abs_offset(int rank, const int64_t* lens, const int64_t* strides) {
+  int64_t s = 0;
+  for (int i = 0; i < rank; ++i)
+    if (lens[i] > 0) s += std::llabs(strides[i]) * (lens[i] - 1);
+  return s;
+}
+
+Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const tc_tensor& C,
+                  Plan* p) {
+  const tc_tensor* T[3] = {&A, &B, &C};
+  if (dtype != TC_F64 && dtype != TC_F32) return Status::err(TC_ERR_ARG, "bad dtype");
+  for (int t = 0; t < 3; ++t) {
+    if (T[t]->rank < 0) return Status::err(TC_ERR_ARG, "negative rank");
+    if (T[t]->rank > TC_MAX_RANK)
+      return Status::err(TC_ERR_UNSUPPORTED, "rank exceeds TC_MAX_RANK");
+    if (T[t]->rank > 0 && (!T[t]->lens || !T[t]->strides || !T[t]->labels))
+      return Status::err(TC_ERR_ARG, "null lens/strides/labels");
+    for (int i = 0; i < T[t]->rank; ++i)
+      if (T[t]->lens[i] < 0) return Status::err(TC_ERR_ARG, "negative length");
+  }
+  Status st = classify(A, B, C, &p->b);
+  if (!st) return st;
+  if (!injective(C.rank, C.lens, C.strides))
+    return Status::err(TC_ERR_ALIAS, "C is not injective (two index tuples share an address)");
+  p->dtype = dtype;
+  p->empty_out = false;
+  for (int i = 0; i < C.rank; ++i)
+    if (C.lens[i] == 0) p->empty_out = true;
+  bool zero_p = false;
+  for (auto& d : p->b.P)
+    if (d.len == 0) zero_p = true;
+  if (zero_p) p->b.P.clear();  // n_P = 0: C := beta*C, modelled as an empty product (k = 0)
+  normalize(&p->b);
+  auto ext = [](const std::vector<Dim>& d) {
+    int64_t n = 1;
+    for (auto& x : d) n *= x.len;
+    return n;
+  };
+  p->m = ext(p->b.I);
+  p->n = ext(p->b.J);
+  p->k = zero_p ? 0 : ext(p->b.P);
+  if (p->empty_out) { p->m = 0; p->n = 0; }
+  // 64-bit offsets only when some tensor spans 2^31 elements or more
+  int64_t big = std::max({max_abs_offset(A.rank, A.lens, A.strides),
+                          max_abs_offset(B.rank, B.lens, B.strides),
+                          max_abs_offset(C.rank, C.lens, C.strides)});
+  p->idx64 = big >= (int64_t(1) << 31) - 1;
+  if (p->m >= (int64_t(1) << 31) || p->n >= (int64_t(1) << 31) || p->k >= (int64_t(1) << 31))
+    return Status::err(TC_ERR_UNSUPPORTED, "a bundle extent exceeds 2^31");
+  if (!p->empty_out) {
+    p->scat[0] = scatter(p->b.I, 0);  // rscat_A
+    p->scat[1] = scatter(p->b.P, 0);  // cscat_A
+    p->scat[2] = scatter(p->b.P, 1);  // rscat_B
+    p->scat[3] = scatter(p->b.J, 0);  // cscat_B
+    p->scat[4] = scatter(p->b.I, 1);  // rscat_C
+    p->scat[5] = scatter(p->b.J, 1);  // cscat_C
+    if (p->k == 0) { p->scat[1].clear(); p->scat[2].clear(); }
+  }
+  // Loader direction per operand: gather along the bundle whose first folded dim has unit
+  // stride (16-byte vectors, coalesced warps); else along the smaller leading stride.
+  auto lead = [](const std::vector<Dim>& d, int w) {
+    return d.empty() ? INT64_MAX : std::llabs(d[0].s[w]);
+  };
+  int64_t a_m = lead(p->b.I, 0), a_k = lead(p->b.P, 0);
+  int64_t b_k = lead(p->b.P, 1), b_n = lead(p->b.J, 0);
+  p->a_vec_m = a_m <= a_k;
+  p->b_vec_k = b_k <= b_n;
+  p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
+               (dtype == TC_F32 ? 8 : 0);
+  return Status::ok();
+}
+
+}  // namespace tcb

@@ -1,0 +1,352 @@
+// C ABI (include/tc.h): validation, plan cache, device tables, host (end-to-end) path.
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "tc.h"
+
+namespace tcb {
+
+static thread_local std::string g_detail;
+
+static int fail(int code, const std::string& detail) {
+  g_detail = detail;
+  return code;
+}
+static int fail(const Status& s) { return fail(s.code, s.detail); }
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(TC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Device copies of a plan's tables on one device.
+struct DeviceTables {
+  int device = -1;
+  void* tab[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  uint8_t* vA = nullptr;
+  uint8_t* vB = nullptr;
+  ~DeviceTables() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& p : tab) cudaFree(p);
+    cudaFree(vA);
+    cudaFree(vB);
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+};
+
+Plan::~Plan() {
+  for (auto* d : dev) delete d;
+}
+
+static int64_t padded(int64_t n) { return ((n + kTablePad - 1) / kTablePad + 1) * kTablePad; }
+
+// Pair flags = block-scatter vector with block size 2, reduced to "stride 1".
+static std::vector<uint8_t> pair_flags(const std::vector<int64_t>& scat, int64_t padlen) {
+  std::vector<int64_t> bs = block_scatter(scat, 2);
+  std::vector<uint8_t> f((size_t)(padlen / 2), 0);
+  for (size_t i = 0; i < bs.size(); ++i) f[i] = (bs[i] == 1 && 2 * i + 1 < scat.size()) ? 1 : 0;
+  return f;
+}
+
+template <typename IDX>
+static cudaError_t upload_table(const std::vector<int64_t>& v, void** out) {
+  int64_t n = padded((int64_t)v.size());
+  std::vector<IDX> h((size_t)n, 0);
+  for (size_t i = 0; i < v.size(); ++i) h[i] = (IDX)v[i];
+  cudaError_t e = cudaMalloc(out, sizeof(IDX) * (size_t)n);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(*out, h.data(), sizeof(IDX) * (size_t)n, cudaMemcpyHostToDevice);
+}
+
+static cudaError_t upload_bytes(const std::vector<uint8_t>& v, uint8_t** out) {
+  cudaError_t e = cudaMalloc((void**)out, v.size() + 16);
+  if (e != cudaSuccess) return e;
+  cudaMemset(*out, 0, v.size() + 16);
+  return cudaMemcpy(*out, v.data(), v.size(), cudaMemcpyHostToDevice);
+}
+
+static int get_tables(const Plan& p, DeviceTables** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(p.mu);
+  for (auto* d : p.dev)
+    if (d->device == dev) { *out = d; return TC_OK; }
+  auto* d = new DeviceTables();
+  d->device = dev;
+  for (int i = 0; i < 6; ++i) {
+    e = p.idx64 ? upload_table<long long>(p.scat[i], &d->tab[i])
+                : upload_table<int>(p.scat[i], &d->tab[i]);
+    if (e != cudaSuccess) { delete d; return cuda_fail(e, "table upload"); }
+  }
+  // A is gathered along rscat_A (M) or cscat_A (K); B along rscat_B (K) or cscat_B (N).
+  const std::vector<int64_t>& ta = p.a_vec_m ? p.scat[0] : p.scat[1];
+  const std::vector<int64_t>& tb = p.b_vec_k ? p.scat[2] : p.scat[3];
+  e = upload_bytes(pair_flags(ta, padded((int64_t)ta.size())), &d->vA);
+  if (e == cudaSuccess) e = upload_bytes(pair_flags(tb, padded((int64_t)tb.size())), &d->vB);
+  if (e != cudaSuccess) { delete d; return cuda_fail(e, "flag upload"); }
+  p.dev.push_back(d);
+  *out = d;
+  return TC_OK;
+}
+
+static int execute(const Plan& p, double alpha, const void* A, const void* B, double beta,
+                   void* C, cudaStream_t stream) {
+  if (p.empty_out || p.m == 0 || p.n == 0) return TC_OK;
+  if (!C) return fail(TC_ERR_ARG, "null C");
+  bool skip_ab = (alpha == 0.0) || p.k == 0;
+  if (!skip_ab && (!A || !B)) return fail(TC_ERR_ARG, "null A or B");
+  size_t esz = p.dtype == TC_F64 ? 8 : 4;
+  for (const void* q : {A, B, (const void*)C})
+    if (q && (reinterpret_cast<uintptr_t>(q) % esz) != 0)
+      return fail(TC_ERR_ARG, "data pointer not aligned to the element size");
+  DeviceTables* d = nullptr;
+  int rc = get_tables(p, &d);
+  if (rc != TC_OK) return rc;
+  LaunchArgs a{};
+  a.A = p.b.swapped ? B : A;  // after heuristic step 4 the roles of A and B are exchanged
+  a.B = p.b.swapped ? A : B;
+  a.C = C;
+  a.rA = d->tab[0]; a.cA = d->tab[1]; a.rB = d->tab[2];
+  a.cB = d->tab[3]; a.rC = d->tab[4]; a.cC = d->tab[5];
+  a.vA = d->vA; a.vB = d->vB;
+  a.M = (int)p.m; a.N = (int)p.n; a.K = skip_ab ? 0 : (int)p.k;
+  a.alpha = alpha; a.beta = beta;
+  a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
+  if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
+  int n = launch_contract(a, stream);
+  if (n == -2) return fail(TC_ERR_UNSUPPORTED, "fp32 kernel not available in this build");
+  if (n < 0) return cuda_fail(cudaGetLastError(), "kernel launch");
+  return TC_OK;
+}
+
+// ---- plan cache --------------------------------------------------------------------------
+
+static std::mutex g_cache_mu;
+static std::map<std::string, std::shared_ptr<Plan>> g_cache;
+
+static void key_tensor(std::string& k, const tc_tensor& t) {
+  k.append(reinterpret_cast<const char*>(&t.rank), sizeof(t.rank));
+  if (t.rank > 0) {
+    k.append(reinterpret_cast<const char*>(t.lens), sizeof(int64_t) * (size_t)t.rank);
+    k.append(reinterpret_cast<const char*>(t.strides), sizeof(int64_t) * (size_t)t.rank);
+    k.append(t.labels, (size_t)t.rank);
+  }
+  k.push_back('|');
+}
+
+static int check_tensor(const tc_tensor* t, const char* name) {
+  if (!t) return fail(TC_ERR_ARG, std::string("null tensor ") + name);
+  if (t->rank < 0) return fail(TC_ERR_ARG, std::string("negative rank in ") + name);
+  if (t->rank > TC_MAX_RANK) return fail(TC_ERR_UNSUPPORTED, std::string("rank > TC_MAX_RANK in ") + name);
+  if (t->rank > 0 && (!t->lens || !t->strides || !t->labels))
+    return fail(TC_ERR_ARG, std::string("null lens/strides/labels in ") + name);
+  return TC_OK;
+}
+
+static int get_plan(tc_dtype dtype, const tc_tensor* A, const tc_tensor* B, const tc_tensor* C,
+                    std::shared_ptr<Plan>* out) {
+  int rc;
+  if ((rc = check_tensor(A, "A")) || (rc = check_tensor(B, "B")) || (rc = check_tensor(C, "C")))
+    return rc;
+  std::string key(1, (char)dtype);
+  key_tensor(key, *A); key_tensor(key, *B); key_tensor(key, *C);
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) { *out = it->second; return TC_OK; }
+  }
+  auto p = std::make_shared<Plan>();
+  Status st = build_plan(dtype, *A, *B, *C, p.get());
+  if (!st) return fail(st);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (g_cache.size() > 4096) g_cache.clear();
+  g_cache.emplace(key, p);
+  *out = p;
+  return TC_OK;
+}
+
+// C must not overlap A or B (reading R7): conservative byte-interval test.
+static bool overlaps(const tc_tensor* X, const tc_tensor* C, size_t esz) {
+  int64_t xl, xh, cl, ch;
+  span(X->rank, X->lens, X->strides, &xl, &xh);
+  span(C->rank, C->lens, C->strides, &cl, &ch);
+  if (xl > xh || cl > ch || !X->data || !C->data) return false;
+  const char* x0 = static_cast<const char*>(X->data) + xl * (int64_t)esz;
+  const char* x1 = static_cast<const char*>(X->data) + (xh + 1) * (int64_t)esz;
+  const char* c0 = static_cast<const char*>(C->data) + cl * (int64_t)esz;
+  const char* c1 = static_cast<const char*>(C->data) + (ch + 1) * (int64_t)esz;
+  return x0 < c1 && c0 < x1;
+}
+
+}  // namespace tcb
+
+using namespace tcb;
+
+extern "C" {
+
+int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
+                double beta, const tc_tensor* C, void* stream) {
+  std::shared_ptr<Plan> p;
+  int rc = get_plan(dtype, A, B, C, &p);
+  if (rc != TC_OK) return rc;
+  size_t esz = dtype == TC_F64 ? 8 : 4;
+  if (overlaps(A, C, esz) || overlaps(B, C, esz))
+    return fail(TC_ERR_ALIAS, "C overlaps A or B");
+  return execute(*p, alpha, A->data, B->data, beta, C->data, static_cast<cudaStream_t>(stream));
+}
+
+int tc_contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
+                     double beta, const tc_tensor* C, void* stream) {
+  std::shared_ptr<Plan> p;
+  int rc = get_plan(dtype, A, B, C, &p);
+  if (rc != TC_OK) return rc;
+  size_t esz = dtype == TC_F64 ? 8 : 4;
+  if (overlaps(A, C, esz) || overlaps(B, C, esz))
+    return fail(TC_ERR_ALIAS, "C overlaps A or B");
+  if (p->empty_out) return TC_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const tc_tensor* T[3] = {A, B, C};
+  void* dbuf[3] = {nullptr, nullptr, nullptr};
+  const char* dbase[3] = {nullptr, nullptr, nullptr};
+  int64_t lo[3], hi[3];
+  bool need_ab = alpha != 0.0 && p->k > 0;
+  cudaError_t e = cudaSuccess;
+  int64_t n_elems_c = 1;
+  for (int i = 0; i < C->rank; ++i) n_elems_c *= C->lens[i];
+  for (int t = 0; t < 3 && e == cudaSuccess; ++t) {
+    span(T[t]->rank, T[t]->lens, T[t]->strides, &lo[t], &hi[t]);
+    if (t < 2 && !need_ab) continue;
+    if (lo[t] > hi[t]) continue;
+    size_t bytes = (size_t)(hi[t] - lo[t] + 1) * esz;
+    if (!T[t]->data) { e = cudaErrorInvalidValue; break; }
+    e = cudaMallocAsync(&dbuf[t], bytes, s);
+    if (e != cudaSuccess) break;
+    dbase[t] = static_cast<const char*>(dbuf[t]) - lo[t] * (int64_t)esz;
+    const char* src = static_cast<const char*>(T[t]->data) + lo[t] * (int64_t)esz;
+    // C's span is uploaded when C is read (beta != 0) or has holes that must survive
+    bool upload = t < 2 || beta != 0.0 || (hi[t] - lo[t] + 1) != n_elems_c;
+    if (upload) e = cudaMemcpyAsync(dbuf[t], src, bytes, cudaMemcpyHostToDevice, s);
+  }
+  if (e == cudaSuccess) {
+    rc = execute(*p, alpha, dbase[0], dbase[1], beta, const_cast<char*>(dbase[2]), s);
+    if (rc == TC_OK && lo[2] <= hi[2]) {
+      size_t bytes = (size_t)(hi[2] - lo[2] + 1) * esz;
+      e = cudaMemcpyAsync(static_cast<char*>(C->data) + lo[2] * (int64_t)esz, dbuf[2], bytes,
+                          cudaMemcpyDeviceToHost, s);
+    }
+  }
+  for (auto* b : dbuf)
+    if (b) cudaFreeAsync(b, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "host path copy");
+  if (rc != TC_OK) return rc;
+  if (e2 != cudaSuccess) return cuda_fail(e2, "host path synchronize");
+  return TC_OK;
+}
+
+int tc_plan_create(tc_plan** plan, tc_dtype dtype, const tc_tensor* A, const tc_tensor* B,
+                   const tc_tensor* C) {
+  if (!plan) return fail(TC_ERR_ARG, "null plan pointer");
+  int rc;
+  if ((rc = check_tensor(A, "A")) || (rc = check_tensor(B, "B")) || (rc = check_tensor(C, "C")))
+    return rc;
+  auto* p = new (std::nothrow) Plan();
+  if (!p) return fail(TC_ERR_NOMEM, "plan allocation");
+  Status st = build_plan(dtype, *A, *B, *C, p);
+  if (!st) { delete p; return fail(st); }
+  *plan = reinterpret_cast<tc_plan*>(p);
+  return TC_OK;
+}
+
+int tc_plan_execute(const tc_plan* plan, double alpha, const void* A, const void* B, double beta,
+                    void* C, void* stream) {
+  if (!plan) return fail(TC_ERR_ARG, "null plan");
+  return execute(*reinterpret_cast<const Plan*>(plan), alpha, A, B, beta, C,
+                 static_cast<cudaStream_t>(stream));
+}
+
+int tc_plan_destroy(tc_plan* plan) {
+  delete reinterpret_cast<Plan*>(plan);
+  return TC_OK;
+}
+
+int tc_plan_query(const tc_plan* plan, tc_plan_info* info) {
+  if (!plan || !info) return fail(TC_ERR_ARG, "null argument");
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  info->m = p.m; info->n = p.n; info->k = p.k;
+  info->flops = 2 * p.m * p.n * p.k;
+  info->swapped = p.b.swapped ? 1 : 0;
+  info->ndims[0] = (int32_t)p.b.I.size();
+  info->ndims[1] = (int32_t)p.b.J.size();
+  info->ndims[2] = (int32_t)p.b.P.size();
+  info->a_vec_m = p.a_vec_m; info->b_vec_k = p.b_vec_k;
+  info->idx64 = p.idx64; info->variant = p.variant;
+  return TC_OK;
+}
+
+int tc_plan_dim(const tc_plan* plan, int which, int idx, int64_t* len, int64_t* s0, int64_t* s1,
+                char* labels, int cap) {
+  if (!plan) return fail(TC_ERR_ARG, "null plan");
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  const std::vector<Dim>* b = which == 0 ? &p.b.I : which == 1 ? &p.b.J : which == 2 ? &p.b.P : nullptr;
+  if (!b || idx < 0 || idx >= (int)b->size()) return fail(TC_ERR_ARG, "bad bundle/dim index");
+  const Dim& d = (*b)[(size_t)idx];
+  if (len) *len = d.len;
+  if (s0) *s0 = d.s[0];
+  if (s1) *s1 = d.s[1];
+  if (labels && cap > 0) {
+    std::snprintf(labels, (size_t)cap, "%s", d.labels.c_str());
+  }
+  return TC_OK;
+}
+
+int tc_plan_scatter(const tc_plan* plan, int which, int64_t* out, int64_t cap, int64_t* len) {
+  if (!plan || which < 0 || which > 5) return fail(TC_ERR_ARG, "bad argument");
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  const auto& v = p.scat[which];
+  if (len) *len = (int64_t)v.size();
+  if (out)
+    for (int64_t i = 0; i < cap && i < (int64_t)v.size(); ++i) out[i] = v[(size_t)i];
+  return TC_OK;
+}
+
+int tc_plan_block_scatter(const tc_plan* plan, int which, int64_t b, int64_t* out, int64_t cap,
+                          int64_t* len) {
+  if (!plan || which < 0 || which > 5 || b <= 0) return fail(TC_ERR_ARG, "bad argument");
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  std::vector<int64_t> bs = block_scatter(p.scat[which], b);
+  if (len) *len = (int64_t)bs.size();
+  if (out)
+    for (int64_t i = 0; i < cap && i < (int64_t)bs.size(); ++i) out[i] = bs[(size_t)i];
+  return TC_OK;
+}
+
+const char* tc_error_string(int code) {
+  switch (code) {
+    case TC_OK: return "ok";
+    case TC_ERR_ARG: return "invalid argument";
+    case TC_ERR_LABEL: return "invalid labels";
+    case TC_ERR_SHAPE: return "length mismatch";
+    case TC_ERR_ALIAS: return "aliasing output";
+    case TC_ERR_UNSUPPORTED: return "unsupported";
+    case TC_ERR_CUDA: return "CUDA error";
+    case TC_ERR_NOMEM: return "out of memory";
+    default: return "unknown error";
+  }
+}
+
+const char* tc_last_error_detail(void) { return g_detail.c_str(); }
+
+int tc_version(void) { return TC_VERSION; }
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element, on the
+same seeded inputs. Tolerance (BASELINE.json north_star): normwise relative error <= 1e-12 for
+fp64 and <= 1e-5 for fp32; bitwise in integer-input mode (pin p5: every partial sum is exact).
+
+Small cases run the full oracle; full BASELINE sizes are checked on sampled sub-blocks (a few
+index values per free label, always including 0 and n-1) that the oracle computes exactly as
+the full contraction would, in the launch configuration bench.py times."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float64: 1e-12, torch.float32: 1e-5}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1607_00291_b200  # noqa: F401  (raises if the native library is missing)
+
+
+def tc():
+    import paper_1607_00291_b200 as m
+    return m
+
+
+def relerr(got, ref):
+    got = np.asarray(got, dtype=np.float64).ravel()
+    ref = np.asarray(ref, dtype=np.float64).ravel()
+    n = np.linalg.norm(ref)
+    d = np.linalg.norm(got - ref)
+    return d / n if n > 0 else d
+
+
+def run_both(case):
+    """Full oracle on CPU and the CUDA path on the same seeded inputs."""
+    A, B, C = W.make_tensors(case, "cpu")
+    Ad, Bd, Cd = W.make_tensors(case, "cuda", gen_device="cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    return Cd.cpu(), ref
+
+
+def check(case, bitwise=False):
+    got, ref = run_both(case)
+    assert torch.isfinite(got).all(), case.name
+    if bitwise:
+        assert torch.equal(got, ref), case.name
+    else:
+        e = relerr(got.numpy(), ref.numpy())
+        assert e <= TOL[case.dtype], (case.name, e)
+    return got, ref
+
+
+def sampled_check(case, Ad, Bd, Cd_before, Cd_after, per_label=3, seed=0):
+    """Check a sampled sub-block of a full-size result: choose `per_label` indices of every free
+    label (incl. 0 and n-1), all indices of every bound label, slice A, B, C to them and run the
+    oracle on the sub-problem (identical arithmetic to the full definition for those elements)."""
+    rs = np.random.RandomState(seed)
+    sel = {}
+    for x in case.lab_c:
+        n = case.lens[x]
+        pick = {0, n - 1} | set(rs.randint(0, n, size=per_label).tolist())
+        sel[x] = torch.tensor(sorted(pick))
+
+    def sub(T, labels):
+        for d, x in enumerate(labels):
+            if x in sel:
+                T = T.index_select(d, sel[x].to(T.device))
+        return T.cpu().contiguous()
+
+    a, b = sub(Ad, case.lab_a), sub(Bd, case.lab_b)
+    c0, c1 = sub(Cd_before, case.lab_c), sub(Cd_after, case.lab_c)
+    ref = c0.clone()
+    oracle.contract(case.spec, a, b, ref, case.alpha, case.beta)
+    return relerr(c1.numpy(), ref.numpy()), c1, ref
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE configs (small enough for the full oracle, or scaled with ragged tails)
+# ---------------------------------------------------------------------------------------------
+
+def test_cfg1_full_nan_C_beta0():
+    got, _ = check(W.cfg1())
+    assert torch.isfinite(got).all()
+
+
+def test_cfg1_integer_bitwise():
+    case = W.cfg1()
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_cfg2_ragged(transposed):
+    case = W.cfg2(transposed).scaled({"m": 300, "n": 257, "k": 333})
+    check(case)
+
+
+@pytest.mark.parametrize("transposed", [False, True])
+def test_cfg2_full_vs_cublas(transposed):
+    """cfg2 at 2048^3: the contraction against cuBLAS DGEMM on the same matrices (P:1216-1238:
+    same flops, same data) and against the oracle on sampled blocks."""
+    case = W.cfg2(transposed)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    Am = Ad if not transposed else Ad.t()     # (m, k)
+    Bm = Bd if not transposed else Bd.t()     # (k, n)
+    ref = case.alpha * (Am @ Bm) + case.beta * C0
+    assert relerr(Cd.cpu().numpy(), ref.cpu().numpy()) < 1e-12
+    e, _, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=40)
+    assert e < 1e-12
+
+
+@pytest.mark.parametrize("variant", [False, True])
+def test_cfg3_scaled(variant):
+    check(W.cfg3(variant, v=24, o=10))
+
+
+@pytest.mark.parametrize("variant", [False, True])
+def test_cfg3_full_sampled(variant):
+    case = W.cfg3(variant)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, _, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=4)
+    assert e < 1e-12
+
+
+def _scaled_cfg4(i, dtype=torch.float64, target=120):
+    case = W.cfg4(i, dtype)
+    lens = {}
+    for x, n in case.lens.items():
+        lens[x] = max(2, int(round(n ** 0.6))) if n > 64 else max(2, n // 3)
+    return case.scaled(lens)
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_cfg4_scaled_f64(i):
+    check(_scaled_cfg4(i))
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_cfg4_full_sampled_f64(i):
+    case = W.cfg4(i)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=3, seed=i)
+    assert torch.isfinite(c1).all()
+    assert e < 1e-12
+
+
+def test_cfg5_scaled_full():
+    check(W.cfg5(big=12, small=6))
+
+
+@pytest.mark.slow
+def test_cfg5_full_sampled():
+    """cfg5 at full size (8.45e13 flops, 30.6 GB), as bench.py runs it at N=1."""
+    case = W.cfg5()
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=2)
+    assert torch.isfinite(c1).all()
+    assert e < 1e-12
+
+
+# ---------------------------------------------------------------------------------------------
+# loader paths, layouts and edge cases
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("spec", ["mn-mk-kn", "mn-km-nk", "mn-mk-nk", "mn-km-kn",
+                                  "nm-mk-kn", "nm-km-nk"])
+def test_all_loader_direction_combinations(spec):
+    lc, la, lb = spec.split("-")
+    case = W.Case("dir_" + spec, lc, la, lb, {"m": 203, "n": 145, "k": 171}, alpha=-0.75,
+                  beta=0.25, c_init="dist", seed=21)
+    check(case)
+    case.dist = "int"
+    case.alpha, case.beta = 2.0, -1.0
+    check(case, bitwise=True)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_small_contractions(seed):
+    case = W.random_tiny_case(seed, max_rank=6, max_len=7)
+    check(case)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_small_integer_bitwise(seed):
+    check(W.random_tiny_case(seed, max_rank=6, max_len=7, dist="int"), bitwise=True)
+
+
+def test_alpha_zero_does_not_read_A_B():
+    case = W.cfg3(False, v=8, o=4)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    Ad.fill_(float("nan")); Bd.fill_(float("nan"))
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, 0.0, 0.5)
+    assert torch.equal(Cd, 0.5 * C0)
+
+
+def test_zero_length_and_empty_bundles():
+    dev = "cuda"
+    A = torch.randn(5, 0, dtype=torch.float64, device=dev)
+    B = torch.randn(0, 7, dtype=torch.float64, device=dev)
+    C = torch.ones(5, 7, dtype=torch.float64, device=dev)
+    tc().contract("mn-mk-kn", A, B, C, 1.0, 0.5)          # n_P = 0 -> C = beta C
+    assert torch.equal(C, torch.full_like(C, 0.5))
+    C0 = torch.ones(0, 7, dtype=torch.float64, device=dev)
+    tc().contract("mn-mk-kn", torch.randn(0, 3, dtype=torch.float64, device=dev),
+                  torch.randn(3, 7, dtype=torch.float64, device=dev), C0, 1.0, 0.0)
+    # outer product (d_P = 0) and full reduction to a scalar (d_I = d_J = 0)
+    for spec, sa, sb, sc in (("ab-a-b", [37], [29], [37, 29]), ("-abc-abc", [5, 6, 7], [5, 6, 7], [])):
+        A = torch.randn(*sa, dtype=torch.float64)
+        B = torch.randn(*sb, dtype=torch.float64)
+        C = torch.zeros(*sc, dtype=torch.float64)
+        ref = C.clone()
+        oracle.contract(spec, A, B, ref, 1.5, 0.0)
+        Cd = C.cuda()
+        tc().contract(spec, A.cuda(), B.cuda(), Cd, 1.5, 0.0)
+        assert relerr(Cd.cpu().numpy(), ref.numpy()) < 1e-13, spec
+
+
+def test_strided_subviews_and_misaligned_bases():
+    """Sub-views with gaps and odd element offsets (16-byte vectors disabled per element)."""
+    rs = torch.Generator().manual_seed(3)
+    bigA = torch.rand(70, 9, 61, dtype=torch.float64, generator=rs)
+    bigB = torch.rand(61, 5, 50, dtype=torch.float64, generator=rs)
+    bigC = torch.rand(71, 53, dtype=torch.float64, generator=rs)
+    for off in (0, 1):
+        A = bigA[off:off + 65, 3, :57]          # (m=65, k=57), strides (549, 1)
+        B = bigB[:57, 2, off:off + 47]           # (k, n=47)
+        C = bigC[off:off + 65, 1:48]             # (m, n)
+        ref = C.clone()
+        oracle.contract("mn-mk-kn", A, B, ref, 1.0, -1.0)
+        Ad = bigA.cuda()[off:off + 65, 3, :57]
+        Bd = bigB.cuda()[:57, 2, off:off + 47]
+        bigCd = bigC.cuda()
+        Cd = bigCd[off:off + 65, 1:48]
+        tc().contract("mn-mk-kn", Ad, Bd, Cd, 1.0, -1.0)
+        assert relerr(Cd.cpu().numpy(), ref.numpy()) < 1e-13
+        # elements of the big buffer outside the view are untouched
+        mask = torch.ones_like(bigC, dtype=torch.bool)
+        mask[off:off + 65, 1:48] = False
+        assert torch.equal(bigCd.cpu()[mask], bigC[mask])
+
+
+def test_storage_permutation_invariance_bitwise():
+    """Permuting an operand's storage with its labels gives identical C (pin p3(i), int mode)."""
+    base = W.Case("perm", "abij", "abef", "efij", {"a": 20, "b": 11, "e": 9, "f": 13, "i": 6, "j": 7},
+                  dist="int", alpha=1.0, beta=0.0, c_init="nan", seed=5)
+    got0, _ = run_both(base)
+    Ad, Bd, _ = W.make_tensors(base, "cuda", gen_device="cpu")
+    for la, perm in (("faeb", (3, 0, 2, 1)), ("ebaf", (2, 1, 0, 3))):
+        A2 = W.colmajor_view(torch.empty(Ad.numel(), dtype=Ad.dtype, device="cuda"),
+                             [base.lens[x] for x in la])
+        A2.copy_(Ad.permute(*perm))
+        C = torch.full([base.lens[x] for x in "abij"], float("nan"), dtype=torch.float64, device="cuda")
+        tc().contract(f"abij-{la}-efij", A2, Bd, C, 1.0, 0.0)
+        assert torch.equal(C.cpu(), got0)
+
+
+def test_errors_raise_and_enqueue_nothing():
+    A = torch.randn(4, 5, dtype=torch.float64, device="cuda")
+    B = torch.randn(5, 6, dtype=torch.float64, device="cuda")
+    C = torch.zeros(4, 6, dtype=torch.float64, device="cuda")
+    with pytest.raises(tc().TCError):
+        tc().contract("mn-mk-kq", A, B, C)
+    with pytest.raises(tc().TCError):
+        tc().contract("mn-mk-kn", A, B, C.as_strided((4, 6), (1, 0)))   # C not injective
+    assert torch.equal(C, torch.zeros_like(C))
+
+
+def test_host_path_end_to_end():
+    case = W.cfg3(True, v=20, o=9)
+    A, B, C = W.make_tensors(case, "cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    Ap, Bp, Cp = A, B, C.clone()
+    tc().contract_host(case.spec, Ap, Bp, Cp, case.alpha, case.beta)
+    assert relerr(Cp.numpy(), ref.numpy()) < 1e-12
+
+
+def test_repeat_calls_bitwise_deterministic():
+    case = W.cfg4(5)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C1, C2 = Cd.clone(), Cd.clone()
+    tc().contract(case.spec, Ad, Bd, C1)
+    tc().contract(case.spec, Ad, Bd, C2)
+    assert torch.equal(C1, C2)

@@ -435,7 +435,7 @@ def test_spec_examples_planner():
     ex = s["fold_and_reorder"][0]
     assert tabs["swapped"] == ex["swapped"]
     # after the swap the roles exchange: new J = old I sorted by C stride -> (b, c, d) = "bcd"
-    # (c,d fold: s_d(C) = 36 = 18*2 = s_c(C)*n_c and s_d(A) = 24 = 8*3 = s_c(A)*n_c -> "cd")
+    # (c, d are contiguous in C but not in A: s_d(A) = 24 != s_c(A)*n_c = 2, so no fold)
     assert "".join(d["labels"] for d in tabs["J"]) == "bcd"
     assert "".join(d["labels"] for d in tabs["I"]) == ex["J_sorted"]
     # partition example: element (0,0) of rows [0,8), cols [8,16) of C with I=cdb, J=ae
