@@ -225,9 +225,9 @@ def test_zero_length_and_empty_bundles():
                   torch.randn(3, 7, dtype=torch.float64, device=dev), C0, 1.0, 0.0)
     # outer product (d_P = 0) and full reduction to a scalar (d_I = d_J = 0)
     for spec, sa, sb, sc in (("ab-a-b", [37], [29], [37, 29]), ("-abc-abc", [5, 6, 7], [5, 6, 7], [])):
-        A = torch.randn(*sa, dtype=torch.float64)
-        B = torch.randn(*sb, dtype=torch.float64)
-        C = torch.zeros(*sc, dtype=torch.float64)
+        A = torch.randn(sa, dtype=torch.float64)
+        B = torch.randn(sb, dtype=torch.float64)
+        C = torch.zeros(sc, dtype=torch.float64)
         ref = C.clone()
         oracle.contract(spec, A, B, ref, 1.5, 0.0)
         Cd = C.cuda()
