@@ -9,8 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtc_b200.so")
-SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu"]
-HEADERS = ["plan.hpp", "kernels.hpp"]
+SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "contract_ws.cu"]
+HEADERS = ["plan.hpp", "kernels.hpp", "dev_common.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

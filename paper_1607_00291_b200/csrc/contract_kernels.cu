@@ -15,9 +15,12 @@
 // epilogue writes alpha*acc + beta*C through rscat_C / cscat_C (beta == 0 never
 // reads C).
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include <cuda_runtime.h>
 
+#include "dev_common.cuh"
 #include "kernels.hpp"
 
 namespace tcb {
@@ -49,33 +52,7 @@ template <bool B_VK> struct BLayout {
   }
 };
 
-__device__ __forceinline__ void cp_async16(double* smem, const double* gmem, bool pred) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-__device__ __forceinline__ bool aligned16(const void* p) {
-  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
-}
-
-// D = A(16x4) * B(4x8) + D, fp64; fragments per CuTe SM90_16x8x4_F64F64F64F64_TN:
-// a0 = A[g][t], a1 = A[g+8][t]; b0 = B[t][g]; d = {C[g][2t], C[g][2t+1], C[g+8][2t], C[g+8][2t+1]}
-__device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b0) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
-      "{%0,%1,%2,%3};\n"
-      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
-      : "d"(a0), "d"(a1), "d"(b0));
-}
+using namespace dev;
 
 // ------------------------------------------------------------------------------------------
 // Operand loaders. A "pair" is two consecutive entries of the table the operand is gathered
@@ -345,10 +322,25 @@ int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+int launch_ws_f64(const LaunchArgs& a, cudaStream_t stream);   // contract_ws.cu
+
+// Kernel selection: the warp-specialised kernel is the default; TC_KERNEL=simple selects the
+// first (non-specialised) kernel for ablation.
+static int kernel_choice() {
+  static int choice = [] {
+    const char* e = getenv("TC_KERNEL");
+    if (e && !strcmp(e, "simple")) return 1;
+    return 0;
+  }();
+  return choice;
+}
+
 int launch_contract(const LaunchArgs& a, cudaStream_t stream) {
   if (a.M <= 0 || a.N <= 0) return 0;
-  if (a.f32) return -2;  // fp32 variant: contract_kernels_f32.cu (not yet built)
-  return a.idx64 ? dispatch_dir<long long>(a, stream) : dispatch_dir<int>(a, stream);
+  if (a.f32) return -2;  // fp32 variant not built yet
+  if (kernel_choice() == 1)
+    return a.idx64 ? dispatch_dir<long long>(a, stream) : dispatch_dir<int>(a, stream);
+  return launch_ws_f64(a, stream);
 }
 
 }  // namespace tcb

@@ -1,0 +1,92 @@
+// Device helpers shared by the contraction kernels (sm_100a, inline PTX).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tcb {
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cp.async with zero-fill: when pred is false no bytes are read and the destination is zeroed.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool pred) {
+  int sz = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(smem)),
+               "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+// ---- mbarrier (CTA scope) -------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+      smem_u32(bar))
+               : "memory");
+}
+// Arrives on `bar` once all prior cp.async operations of this thread have completed; the
+// arrival counts against the barrier's expected count (.noinc).
+__device__ __forceinline__ void mbar_cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---- FP64 tensor core (DMMA) ----------------------------------------------------------------
+// D = A(16x4) * B(4x8) + D, fp64; fragments per CuTe SM90_16x8x4_F64F64F64F64_TN:
+// a0 = A[g][t], a1 = A[g+8][t]; b0 = B[t][g]; d = {C[g][2t], C[g][2t+1], C[g+8][2t], C[g+8][2t+1]}
+// (g = lane / 4, t = lane % 4). Lowers to two DMMA.8x8x4 on sm_100a.
+__device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Tile rasterisation: GROUP_M consecutive M-tiles walk the N-tiles together so that CTAs
+// running at the same time share A and B panels in L2.
+template <int GROUP_M>
+__device__ __forceinline__ void tile_coords(int pid, int tiles_m, int tiles_n, int* tm, int* tn) {
+  const int group_size = GROUP_M * tiles_n;
+  const int first_m = (pid / group_size) * GROUP_M;
+  const int gm = min(tiles_m - first_m, GROUP_M);
+  *tm = first_m + (pid % group_size) % gm;
+  *tn = (pid % group_size) / gm;
+}
+
+}  // namespace dev
+}  // namespace tcb

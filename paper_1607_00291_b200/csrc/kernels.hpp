@@ -27,6 +27,8 @@ struct LaunchArgs {
   int M, N, K;
   double alpha, beta;
   bool a_vec_m, b_vec_k, idx64, f32;
+  // every pair of the operand's gather direction is contiguous and 16-byte aligned
+  bool a_vec_all, b_vec_all;
 };
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).

@@ -179,6 +179,20 @@ void span(int rank, const int64_t* lens, const int64_t* strides, int64_t* lo, in
   *lo = a; *hi = b;
 }
 
+// True when every block of 2 entries of `vtab` is contiguous (block-scatter entry 1,
+// P:678-683), vtab has even length, and every pair start and every entry of `other` is even
+// -- then base + vtab[2i] + other[r] (and the zero-fill addresses of padded rows, whose table
+// entries are 0) is 16-byte aligned for a 16-byte aligned base, and the kernel moves each pair
+// with one 16-byte copy without per-element checks.
+static bool vec_pairs_all(const std::vector<int64_t>& vtab, const std::vector<int64_t>& other) {
+  if (vtab.empty() || other.empty() || vtab.size() % 2) return false;
+  for (size_t i = 0; i < vtab.size(); i += 2)
+    if (vtab[i + 1] != vtab[i] + 1 || (vtab[i] & 1)) return false;
+  for (int64_t x : other)
+    if (x & 1) return false;
+  return true;
+}
+
 static int64_t max_abs_offset(int rank, const int64_t* lens, const int64_t* strides) {
   int64_t s = 0;
   for (int i = 0; i < rank; ++i)
@@ -246,6 +260,12 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   int64_t b_k = lead(p->b.P, 1), b_n = lead(p->b.J, 0);
   p->a_vec_m = a_m <= a_k;
   p->b_vec_k = b_k <= b_n;
+  if (!p->empty_out && p->k > 0) {
+    p->a_pairs_all = p->a_vec_m ? vec_pairs_all(p->scat[0], p->scat[1])
+                                : vec_pairs_all(p->scat[1], p->scat[0]);
+    p->b_pairs_all = p->b_vec_k ? vec_pairs_all(p->scat[2], p->scat[3])
+                                : vec_pairs_all(p->scat[3], p->scat[2]);
+  }
   p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
                (dtype == TC_F32 ? 8 : 0);
   return Status::ok();

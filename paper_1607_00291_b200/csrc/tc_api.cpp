@@ -122,6 +122,8 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.M = (int)p.m; a.N = (int)p.n; a.K = skip_ab ? 0 : (int)p.k;
   a.alpha = alpha; a.beta = beta;
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
+  a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0;
+  a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0;
   if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
   int n = launch_contract(a, stream);
   if (n == -2) return fail(TC_ERR_UNSUPPORTED, "fp32 kernel not available in this build");
