@@ -322,10 +322,10 @@ int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-int launch_ws_f64(const LaunchArgs& a, cudaStream_t stream);   // contract_ws.cu
+int launch_ws(const LaunchArgs& a, cudaStream_t stream);   // contract_ws.cu
 
-// Kernel selection: the warp-specialised kernel is the default; TC_KERNEL=simple selects the
-// first (non-specialised) kernel for ablation.
+// Kernel selection: the warp-specialised kernel (contract_ws.cu, fp64 and fp32) is the default;
+// TC_KERNEL=simple selects the first (non-specialised, fp64-only) kernel for ablation.
 static int kernel_choice() {
   static int choice = [] {
     const char* e = getenv("TC_KERNEL");
@@ -337,10 +337,9 @@ static int kernel_choice() {
 
 int launch_contract(const LaunchArgs& a, cudaStream_t stream) {
   if (a.M <= 0 || a.N <= 0) return 0;
-  if (a.f32) return -2;  // fp32 variant not built yet
-  if (kernel_choice() == 1)
+  if (kernel_choice() == 1 && !a.f32)
     return a.idx64 ? dispatch_dir<long long>(a, stream) : dispatch_dir<int>(a, stream);
-  return launch_ws_f64(a, stream);
+  return launch_ws(a, stream);
 }
 
 }  // namespace tcb

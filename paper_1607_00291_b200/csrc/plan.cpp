@@ -179,17 +179,22 @@ void span(int rank, const int64_t* lens, const int64_t* strides, int64_t* lo, in
   *lo = a; *hi = b;
 }
 
-// True when every block of 2 entries of `vtab` is contiguous (block-scatter entry 1,
-// P:678-683), vtab has even length, and every pair start and every entry of `other` is even
-// -- then base + vtab[2i] + other[r] (and the zero-fill addresses of padded rows, whose table
-// entries are 0) is 16-byte aligned for a 16-byte aligned base, and the kernel moves each pair
-// with one 16-byte copy without per-element checks.
-static bool vec_pairs_all(const std::vector<int64_t>& vtab, const std::vector<int64_t>& other) {
-  if (vtab.empty() || other.empty() || vtab.size() % 2) return false;
-  for (size_t i = 0; i < vtab.size(); i += 2)
-    if (vtab[i + 1] != vtab[i] + 1 || (vtab[i] & 1)) return false;
+// True when every block of V entries of `vtab` is contiguous (block-scatter entry 1 with block
+// size V), vtab's length is a multiple of V, and every block start and every entry
+// of `other` is a multiple of V -- then base + vtab[V i] + other[r] (and the zero-fill
+// addresses of padded rows, whose table entries are 0) is 16-byte aligned for a 16-byte
+// aligned base (V = 16 / element size), and the kernel moves each block with one 16-byte copy
+// without per-element checks.
+static bool vec_blocks_all(const std::vector<int64_t>& vtab, const std::vector<int64_t>& other,
+                           int64_t V) {
+  if (vtab.empty() || other.empty() || vtab.size() % (size_t)V) return false;
+  for (size_t i = 0; i < vtab.size(); i += (size_t)V) {
+    if (vtab[i] % V) return false;
+    for (int64_t j = 1; j < V; ++j)
+      if (vtab[i + (size_t)j] != vtab[i] + j) return false;
+  }
   for (int64_t x : other)
-    if (x & 1) return false;
+    if (x % V) return false;
   return true;
 }
 
@@ -261,10 +266,11 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   p->a_vec_m = a_m <= a_k;
   p->b_vec_k = b_k <= b_n;
   if (!p->empty_out && p->k > 0) {
-    p->a_pairs_all = p->a_vec_m ? vec_pairs_all(p->scat[0], p->scat[1])
-                                : vec_pairs_all(p->scat[1], p->scat[0]);
-    p->b_pairs_all = p->b_vec_k ? vec_pairs_all(p->scat[2], p->scat[3])
-                                : vec_pairs_all(p->scat[3], p->scat[2]);
+    const int64_t V = dtype == TC_F64 ? 2 : 4;
+    p->a_pairs_all = p->a_vec_m ? vec_blocks_all(p->scat[0], p->scat[1], V)
+                                : vec_blocks_all(p->scat[1], p->scat[0], V);
+    p->b_pairs_all = p->b_vec_k ? vec_blocks_all(p->scat[2], p->scat[3], V)
+                                : vec_blocks_all(p->scat[3], p->scat[2], V);
   }
   p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
                (dtype == TC_F32 ? 8 : 0);

@@ -64,7 +64,7 @@ struct Plan {
   bool a_vec_m = true;     // loader direction of A (true: along M)
   bool b_vec_k = true;     // loader direction of B (true: along K)
   bool idx64 = false;
-  // block-scatter check at pair granularity over a whole operand (see vec_pairs_all)
+  // whole-operand block-scatter check at 16-byte granularity (see vec_blocks_all in plan.cpp)
   bool a_pairs_all = false, b_pairs_all = false;
   int variant = 0;
   // per-device uploaded tables

@@ -49,11 +49,14 @@ Plan::~Plan() {
 
 static int64_t padded(int64_t n) { return ((n + kTablePad - 1) / kTablePad + 1) * kTablePad; }
 
-// Pair flags = block-scatter vector with block size 2, reduced to "stride 1".
-static std::vector<uint8_t> pair_flags(const std::vector<int64_t>& scat, int64_t padlen) {
-  std::vector<int64_t> bs = block_scatter(scat, 2);
-  std::vector<uint8_t> f((size_t)(padlen / 2), 0);
-  for (size_t i = 0; i < bs.size(); ++i) f[i] = (bs[i] == 1 && 2 * i + 1 < scat.size()) ? 1 : 0;
+// Vector flags = block-scatter vector with block size V = 16 / element size,
+// reduced to "this block of V entries is V consecutive addresses" (a short tail block is 0).
+static std::vector<uint8_t> vec_flags(const std::vector<int64_t>& scat, int64_t padlen,
+                                      int64_t V) {
+  std::vector<int64_t> bs = block_scatter(scat, V);
+  std::vector<uint8_t> f((size_t)(padlen / V + 1), 0);
+  for (size_t i = 0; i < bs.size(); ++i)
+    f[i] = (bs[i] == 1 && (int64_t)(i + 1) * V <= (int64_t)scat.size()) ? 1 : 0;
   return f;
 }
 
@@ -91,8 +94,9 @@ static int get_tables(const Plan& p, DeviceTables** out) {
   // A is gathered along rscat_A (M) or cscat_A (K); B along rscat_B (K) or cscat_B (N).
   const std::vector<int64_t>& ta = p.a_vec_m ? p.scat[0] : p.scat[1];
   const std::vector<int64_t>& tb = p.b_vec_k ? p.scat[2] : p.scat[3];
-  e = upload_bytes(pair_flags(ta, padded((int64_t)ta.size())), &d->vA);
-  if (e == cudaSuccess) e = upload_bytes(pair_flags(tb, padded((int64_t)tb.size())), &d->vB);
+  const int64_t V = p.dtype == TC_F64 ? 2 : 4;
+  e = upload_bytes(vec_flags(ta, padded((int64_t)ta.size()), V), &d->vA);
+  if (e == cudaSuccess) e = upload_bytes(vec_flags(tb, padded((int64_t)tb.size()), V), &d->vB);
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "flag upload"); }
   p.dev.push_back(d);
   *out = d;
@@ -126,7 +130,6 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0;
   if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
   int n = launch_contract(a, stream);
-  if (n == -2) return fail(TC_ERR_UNSUPPORTED, "fp32 kernel not available in this build");
   if (n < 0) return cuda_fail(cudaGetLastError(), "kernel launch");
   return TC_OK;
 }

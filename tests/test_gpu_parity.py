@@ -302,3 +302,57 @@ def test_repeat_calls_bitwise_deterministic():
     tc().contract(case.spec, Ad, Bd, C1)
     tc().contract(case.spec, Ad, Bd, C2)
     assert torch.equal(C1, C2)
+
+
+# ---------------------------------------------------------------------------------------------
+# fp32 (cfg4's fp32 half): operands widened to fp64 in the micro-kernel, rounded once (R12)
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("i", range(20))
+def test_cfg4_scaled_f32(i):
+    check(_scaled_cfg4(i, torch.float32))
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_cfg4_full_sampled_f32(i):
+    case = W.cfg4(i, torch.float32)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=3, seed=i)
+    assert torch.isfinite(c1).all()
+    assert e < TOL[torch.float32]
+
+
+@pytest.mark.parametrize("spec", ["mn-mk-kn", "mn-km-nk", "mn-mk-nk", "mn-km-kn"])
+@pytest.mark.parametrize("mnk", [(203, 145, 171), (256, 128, 64)])
+def test_f32_loader_directions(spec, mnk):
+    lc, la, lb = spec.split("-")
+    case = W.Case("f32dir_" + spec, lc, la, lb, dict(zip("mnk", mnk)), dtype=torch.float32,
+                  alpha=-0.75, beta=0.25, c_init="dist", seed=22)
+    check(case)
+    case.dist = "int"
+    case.alpha, case.beta = 2.0, -1.0
+    check(case, bitwise=True)
+
+
+@pytest.mark.parametrize("seed", range(15))
+def test_random_small_f32(seed):
+    check(W.random_tiny_case(seed, max_rank=6, max_len=7, dtype=torch.float32))
+
+
+def test_f32_misaligned_views():
+    g = torch.Generator().manual_seed(4)
+    bigA = torch.rand(70, 9, 61, generator=g)
+    bigB = torch.rand(61, 5, 50, generator=g)
+    bigC = torch.rand(71, 53, generator=g)
+    for off in (0, 1, 2, 3):
+        A = bigA[off:off + 65, 3, :57]
+        B = bigB[:57, 2, off:off + 47]
+        C = bigC[off:off + 65, 1:48]
+        ref = C.clone()
+        oracle.contract("mn-mk-kn", A, B, ref, 1.0, -1.0)
+        Cd = bigC.cuda()[off:off + 65, 1:48]
+        tc().contract("mn-mk-kn", bigA.cuda()[off:off + 65, 3, :57],
+                      bigB.cuda()[:57, 2, off:off + 47], Cd, 1.0, -1.0)
+        assert relerr(Cd.cpu().numpy(), ref.numpy()) < 1e-6
