@@ -100,9 +100,9 @@ class Desc:
 
 def _dtype_code(dtype) -> int:
     import torch
-    if dtype == torch.float64:
+    if dtype is torch.float64:
         return TC_F64
-    if dtype == torch.float32:
+    if dtype is torch.float32:
         return TC_F32
     raise TypeError(f"unsupported dtype {dtype}")
 
@@ -115,14 +115,29 @@ def parse_spec(spec: str) -> Tuple[str, str, str]:
     return parts[0], parts[1], parts[2]
 
 
-def _desc(t, labels: str) -> Desc:
-    return Desc(labels, list(t.shape), list(t.stride()), t.data_ptr())
+_tls = __import__("threading").local()
+
+
+def _desc(t, labels: str, role: int = 0) -> Desc:
+    """Descriptor of a torch tensor; the lens/strides arrays are cached per thread by
+    (operand role, labels, shape, strides) so repeated calls only refresh the data pointer."""
+    cache = getattr(_tls, "descs", None)
+    if cache is None:
+        cache = _tls.descs = {}
+    key = (role, labels, t.shape, t.stride())
+    d = cache.get(key)
+    if d is None:
+        if len(cache) > 256:
+            cache.clear()
+        d = cache[key] = Desc(labels, list(t.shape), list(t.stride()), 0)
+    d.t.data = t.data_ptr()
+    return d
 
 
 def _stream_ptr(stream) -> Optional[int]:
     import torch
     if stream is None:
-        stream = torch.cuda.current_stream()
+        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
     return stream.cuda_stream
 
 
@@ -140,15 +155,20 @@ def tc_contract_host(dtype: int, alpha: float, A: Desc, B: Desc, beta: float, C:
                                  float(beta), ctypes.byref(C.t), stream))
 
 
+_specs = {}
+
+
 def contract(spec: str, A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
     """C := alpha * A.B + beta * C for torch CUDA tensors, asynchronously on `stream`
     (default: the current torch stream). Returns C."""
-    lc, la, lb = parse_spec(spec)
-    for t in (A, B, C):
-        if not t.is_cuda:
-            raise ValueError("contract() takes CUDA tensors; use contract_host() for host memory")
-    tc_contract(_dtype_code(C.dtype), alpha, _desc(A, la), _desc(B, lb), beta, _desc(C, lc),
-                _stream_ptr(stream))
+    labels = _specs.get(spec)
+    if labels is None:
+        labels = _specs[spec] = parse_spec(spec)
+    lc, la, lb = labels
+    if not (A.is_cuda and B.is_cuda and C.is_cuda):
+        raise ValueError("contract() takes CUDA tensors; use contract_host() for host memory")
+    tc_contract(_dtype_code(C.dtype), alpha, _desc(A, la, 0), _desc(B, lb, 1), beta,
+                _desc(C, lc, 2), _stream_ptr(stream))
     return C
 
 
@@ -156,8 +176,8 @@ def contract_host(spec: str, A, B, C, alpha: float = 1.0, beta: float = 0.0, str
     """End-to-end path on host tensors (pinned for full bandwidth): the library copies the
     operands to the current CUDA device, contracts, and copies C back (synchronous)."""
     lc, la, lb = parse_spec(spec)
-    tc_contract_host(_dtype_code(C.dtype), alpha, _desc(A, la), _desc(B, lb), beta,
-                     _desc(C, lc), _stream_ptr(stream))
+    tc_contract_host(_dtype_code(C.dtype), alpha, _desc(A, la, 0), _desc(B, lb, 1), beta,
+                     _desc(C, lc, 2), _stream_ptr(stream))
     return C
 
 
@@ -180,7 +200,7 @@ class Plan:
                    (list(A.stride()), list(B.stride()), list(C.stride())))
 
     def __del__(self):
-        if getattr(self, "_p", None) and self._p.value:
+        if getattr(self, "_p", None) and self._p.value and _lib is not None:
             _lib.tc_plan_destroy(self._p)
             self._p = ctypes.c_void_p()
 

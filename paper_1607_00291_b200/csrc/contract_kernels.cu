@@ -326,19 +326,24 @@ int launch_ws(const LaunchArgs& a, cudaStream_t stream);   // contract_ws.cu
 
 // Kernel selection: the warp-specialised kernel (contract_ws.cu, fp64 and fp32) is the default;
 // TC_KERNEL=simple selects the first (non-specialised, fp64-only) kernel for ablation.
+// TC_KERNEL=ws_nosk keeps the persistent kernel but turns off its stream-K tail.
 static int kernel_choice() {
   static int choice = [] {
     const char* e = getenv("TC_KERNEL");
     if (e && !strcmp(e, "simple")) return 1;
+    if (e && !strcmp(e, "ws_nosk")) return 2;
     return 0;
   }();
   return choice;
 }
 
-int launch_contract(const LaunchArgs& a, cudaStream_t stream) {
-  if (a.M <= 0 || a.N <= 0) return 0;
-  if (kernel_choice() == 1 && !a.f32)
-    return a.idx64 ? dispatch_dir<long long>(a, stream) : dispatch_dir<int>(a, stream);
+int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
+  if (args.M <= 0 || args.N <= 0) return 0;
+  const int choice = kernel_choice();
+  if (choice == 1 && !args.f32)
+    return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
+  LaunchArgs a = args;
+  a.stream_k = choice != 2;
   return launch_ws(a, stream);
 }
 

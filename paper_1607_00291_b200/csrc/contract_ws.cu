@@ -37,6 +37,10 @@ constexpr int NTHREADS = (NCW + NPW) * 32;
 constexpr int WM = 64, WN = 32;
 constexpr int STAGES = 4;
 constexpr int GROUP_M = 8;
+// setmaxnreg budgets: 128 x 56 + 256 x 224 = 64512 <= 65536 registers per SM, and per SMSP
+// (warps w, w+4, w+8) 224 + 224 + 56 = 504 <= 512 registers per lane.
+constexpr int kProducerRegs = 64;
+constexpr int kConsumerRegs = 216;
 
 // Row pads (elements). Fragment loads read 8 rows x 4 columns per half-warp (fp64) or per warp
 // (fp32); these pads make every load conflict free: [k][m] rows need LD = 4 mod 16 doubles /
@@ -168,6 +172,66 @@ struct Gather {
   }
 };
 
+// ------------------------------------------------------------------------------------------
+// Persistent schedule: data-parallel full waves + a stream-K tail.
+// Tiles [0, D) are whole tiles, dealt round-robin (CTA w takes w, w+P, ...), so CTAs running at
+// the same time work on consecutive tiles (L2 reuse through the grouped rasterisation). The
+// last S = T - D tiles are split by K iterations evenly over P_sk CTAs (stream-K), which removes
+// the wave-quantisation loss of the final partial wave. Each CTA walks its stream-K range in
+// REVERSE tile order, so the k-first piece of every split tile is computed at the start of the
+// tail and its k-last piece at the end: the first piece writes alpha*acc + beta*C, later pieces
+// add alpha*acc in a fixed order behind a per-tile flag. No partial-sum workspace, deterministic
+// results, and a piece only waits on lower-ranked CTAs' first work items (no deadlock).
+// ------------------------------------------------------------------------------------------
+struct Sched {
+  int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
+  int P_sk;                 // CTAs in the stream-K tail (0: no tail)
+  long long I;              // stream-K iterations = (T - D) * KT
+};
+
+struct WorkIter {
+  int dp_t, D, P, KT;
+  int sk_t, sk_lo;          // current / lowest stream-K tile (relative to D), descending
+  long long g0, g1;         // this CTA's stream-K iteration range
+
+  __device__ __forceinline__ void init(const Sched& s, int w) {
+    D = s.D; P = s.P; KT = s.KT;
+    dp_t = w < s.P ? w : s.D;
+    sk_t = -1; sk_lo = 0; g0 = g1 = 0;
+    if (w < s.P_sk) {
+      g0 = (long long)w * s.I / s.P_sk;
+      g1 = (long long)(w + 1) * s.I / s.P_sk;
+      if (g1 > g0) { sk_t = (int)((g1 - 1) / KT); sk_lo = (int)(g0 / KT); }
+    }
+  }
+  // next work item: tile index, K-iteration range [kb, ke), stream-K piece flag
+  __device__ __forceinline__ bool next(int& tile, int& kb, int& ke, bool& sk) {
+    if (dp_t < D) { tile = dp_t; dp_t += P; kb = 0; ke = KT; sk = false; return true; }
+    if (sk_t >= sk_lo) {
+      const long long base = (long long)sk_t * KT;
+      kb = (int)(g0 > base ? g0 - base : 0);
+      ke = (int)(g1 - base < KT ? g1 - base : KT);
+      tile = D + sk_t;
+      --sk_t;
+      sk = true;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
+}
+
 template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
@@ -175,7 +239,8 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
                   const IDX* __restrict__ rB, const IDX* __restrict__ cB,
                   const IDX* __restrict__ rC, const IDX* __restrict__ cC,
                   const uint8_t* __restrict__ vA, const uint8_t* __restrict__ vB,
-                  int M, int N, int K, int tiles_m, int tiles_n, double alpha, double beta) {
+                  int M, int N, int K, int tiles_m, int tiles_n, double alpha, double beta,
+                  Sched sched, int* __restrict__ flags) {
   using AL = ALay<T, A_VM>;
   using BL = BLay<T, B_VK>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -185,11 +250,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       smem_raw + ((STAGES * (AL::STAGE + BL::STAGE) * sizeof(T) + 15) / 16) * 16);
   uint64_t* empty = full + STAGES;
 
-  int tm, tn;
-  tile_coords<GROUP_M>(blockIdx.x, tiles_m, tiles_n, &tm, &tn);
-  const int m0 = tm * BM, n0 = tn * BN;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KT = (K + BK - 1) / BK;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -200,96 +261,196 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
   }
   __syncthreads();
 
+  WorkIter wi;
+  wi.init(sched, blockIdx.x);
+  int tile, kb, ke;
+  bool sk;
+  uint32_t it = 0;   // global K-iteration counter of this CTA: ring stage and phase
+
   if (warp >= NCW) {
     // ------------------------------- producers -------------------------------
+    // registers move from the producer warpgroup to the two consumer warpgroups
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     const int p = threadIdx.x - NCW * 32;
     Gather<T, IDX, A_VM, A_VEC, AL::LD> ga;
     Gather<T, IDX, !B_VK, B_VEC, BL::LD> gb;
-    // A's tile bundle is M (rA), B's is N (cB); their K tables are cA and rB.
-    ga.init(rA, vA, m0, M, p);
-    gb.init(cB, vB, n0, N, p);
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-      ga.issue(As + s * AL::STAGE, A, cA, vA, kt * BK, K, p);
-      gb.issue(Bs + s * BL::STAGE, B, rB, vB, kt * BK, K, p);
-      mbar_cp_async_arrive(&full[s]);
+    while (wi.next(tile, kb, ke, sk)) {
+      int tm, tn;
+      tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
+      // A's tile bundle is M (rA), B's is N (cB); their K tables are cA and rB.
+      ga.init(rA, vA, tm * BM, M, p);
+      gb.init(cB, vB, tn * BN, N, p);
+      for (int kt = kb; kt < ke; ++kt, ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        ga.issue(As + s * AL::STAGE, A, cA, vA, kt * BK, K, p);
+        gb.issue(Bs + s * BL::STAGE, B, rB, vB, kt * BK, K, p);
+        mbar_cp_async_arrive(&full[s]);
+      }
     }
     cp_async_wait_all();
     return;
   }
 
   // --------------------------------- consumers ---------------------------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 1) * WM, wn = (warp >> 1) * WN;
-  double acc[4][4][4];
+  while (wi.next(tile, kb, ke, sk)) {
+    int tm, tn;
+    tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
+    const int m0 = tm * BM, n0 = tn * BN;
+    if (beta != 0.0 && kb == 0 && ke - kb >= 4) {
+      // pull the warp's 64 x 32 block of C into L2 while the K loop runs: lane l takes column
+      // l and four 16-row runs (one 128-byte line each when C is contiguous along M)
+      const int n = n0 + wn + lane;
+      if (n < N) {
+        const IDX c = cC[n];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
-
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const T* as = As + s * AL::STAGE;
-    const T* bs = Bs + s * BL::STAGE;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[4][2], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a[i][0] = static_cast<double>(as[AL::at(wm + 16 * i + g, 4 * kk + t)]);
-        a[i][1] = static_cast<double>(as[AL::at(wm + 16 * i + g + 8, 4 * kk + t)]);
+        for (int q = 0; q < 4; ++q) {
+          const int m = m0 + wm + 16 * q;
+          if (m < M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + (rC[m] + c)));
+        }
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = static_cast<double>(bs[BL::at(4 * kk + t, wn + 8 * j + g)]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-
-  // epilogue: C[rC[m] + cC[n]] = alpha*acc + beta*C (beta == 0: C not read); computed in fp64,
-  // rounded once to T
-  IDX rc[8], cc[8];
-  int mm[8], nn[8];
+    double acc[4][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = m0 + wm + 16 * i + g + 8 * h;
-      mm[2 * i + h] = m;
-      rc[2 * i + h] = rC[m];
-    }
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int n = n0 + wn + 8 * j + 2 * t + e;
-      nn[2 * j + e] = n;
-      cc[2 * j + e] = cC[n];
-    }
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (mm[2 * i + h] >= M) continue;
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (nn[2 * j + e] >= N) continue;
-          T* q = C + (rc[2 * i + h] + cc[2 * j + e]);
-          double v = alpha * acc[i][j][2 * h + e];
-          if (beta != 0.0) v = fma(beta, static_cast<double>(*q), v);
-          *q = static_cast<T>(v);
+        for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    for (int kt = kb; kt < ke; ++kt, ++it) {
+      const int s = it % STAGES;
+      mbar_wait(&full[s], (it / STAGES) & 1);
+      const T* as = As + s * AL::STAGE;
+      const T* bs = Bs + s * BL::STAGE;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double a[4][2], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a[i][0] = static_cast<double>(as[AL::at(wm + 16 * i + g, 4 * kk + t)]);
+          a[i][1] = static_cast<double>(as[AL::at(wm + 16 * i + g + 8, 4 * kk + t)]);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          b[j] = static_cast<double>(bs[BL::at(4 * kk + t, wn + 8 * j + g)]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
     }
+
+    // stream-K piece order: piece 0 (kb == 0) writes alpha*acc + beta*C; piece j >= 1 waits
+    // for flag == j and adds alpha*acc; a piece that is not the last publishes flag = j + 1.
+    const bool split = sk && !(kb == 0 && ke == sched.KT);
+    int piece = 0;
+    int* flag = nullptr;
+    if (split) {
+      const int s_local = tile - sched.D;
+      const long long g_first = (long long)s_local * sched.KT;
+      const int owner = (int)(((g_first + 1) * sched.P_sk + sched.I - 1) / sched.I) - 1;
+      piece = blockIdx.x - owner;
+      flag = flags + s_local;
+      if (piece > 0) {
+        if (threadIdx.x == 0)
+          while (ld_acquire(flag) != piece) __nanosleep(100);
+        consumers_sync();
+      }
+    }
+    const bool accumulate = split && piece > 0;
+
+    // epilogue: C[rC[m] + cC[n]] = alpha*acc + beta*C (beta == 0: C not read); computed in
+    // fp64, rounded once to T. C is read in chunks of 16 independent loads (one m16 row block)
+    // so the loads of a chunk overlap instead of each waiting behind the previous store.
+    IDX cc[8];
+    int nn[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn + 8 * j + 2 * t + e;
+        nn[2 * j + e] = n;
+        cc[2 * j + e] = cC[n];
+      }
+    const bool read_c = accumulate || beta != 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int mm[2];
+      IDX rc[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        mm[h] = m0 + wm + 16 * i + g + 8 * h;
+        rc[h] = rC[mm[h]];
+      }
+      double old[2][4][2];
+      if (read_c) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              old[h][j][e] = 0.0;
+              if (mm[h] < M && nn[2 * j + e] < N) {
+                const T* q = C + (rc[h] + cc[2 * j + e]);
+                old[h][j][e] = static_cast<double>(accumulate ? __ldcg(q) : *q);
+              }
+            }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (mm[h] >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (nn[2 * j + e] >= N) continue;
+            double v = alpha * acc[i][j][2 * h + e];
+            if (accumulate) v += old[h][j][e];
+            else if (beta != 0.0) v = fma(beta, old[h][j][e], v);
+            C[rc[h] + cc[2 * j + e]] = static_cast<T>(v);
+          }
+      }
+    }
+    if (split) {
+      // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
+      // again when the kernel ends (no per-launch reset)
+      consumers_sync();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(flag, ke < sched.KT ? piece + 1 : 0);
+      }
+    }
+  }
+}
+
+// Host side of the schedule: D whole tiles round-robin over P = #SMs CTAs, the rest split by
+// K iterations over P_sk CTAs (each gets >= kMinSkIters iterations). TC_KERNEL=ws_nosk turns
+// the tail off (all tiles data-parallel) for ablation.
+constexpr int kMinSkIters = 8;
+constexpr int kMaxPieces = 16;   // at most this many stream-K pieces per tile (fix-up chain)
+
+static Sched make_sched(int T, int KT, int nsm, bool allow_sk) {
+  Sched s{};
+  s.T = T; s.KT = KT; s.P = nsm;
+  int D;
+  if (!allow_sk || KT == 0 || T % nsm == 0) D = T;
+  else if (T < nsm) D = 0;
+  else D = (T / nsm - 1) * nsm;
+  s.D = D;
+  s.I = (long long)(T - D) * KT;
+  long long psk = s.I / kMinSkIters;   // each stream-K CTA gets >= kMinSkIters iterations
+  if (psk < 1) psk = 1;
+  if (psk > nsm) psk = nsm;
+  if (psk > (long long)(T - D) * kMaxPieces) psk = (long long)(T - D) * kMaxPieces;
+  s.P_sk = D < T ? (int)psk : 0;
+  return s;
 }
 
 template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC>
@@ -306,13 +467,22 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
     attr_set = true;
   }
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
-  kern<<<tiles_m * tiles_n, NTHREADS, smem, stream>>>(
+  const int KT = (a.K + BK - 1) / BK;
+  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k);
+  if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) {   // cannot happen: S < 2 * num_sms
+    Sched dp = make_sched(tiles_m * tiles_n, KT, a.num_sms, false);
+    sc = dp;
+  }
+  int* flags = a.flags;
+  const int grid = sc.D > 0 ? sc.P : sc.P_sk;
+  kern<<<grid, NTHREADS, smem, stream>>>(
       static_cast<const T*>(a.A), static_cast<const T*>(a.B), static_cast<T*>(a.C),
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
       static_cast<const IDX*>(a.rB), static_cast<const IDX*>(a.cB),
       static_cast<const IDX*>(a.rC), static_cast<const IDX*>(a.cC), a.vA, a.vB, a.M, a.N, a.K,
-      tiles_m, tiles_n, a.alpha, a.beta);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+      tiles_m, tiles_n, a.alpha, a.beta, sc, flags);
+  if (cudaPeekAtLastError() != cudaSuccess) return -1;
+  return 1;
 }
 
 template <typename T, typename IDX, bool A_VEC, bool B_VEC>

@@ -29,6 +29,10 @@ struct LaunchArgs {
   bool a_vec_m, b_vec_k, idx64, f32;
   // every pair of the operand's gather direction is contiguous and 16-byte aligned
   bool a_vec_all, b_vec_all;
+  int num_sms;        // persistent grid size (SMs of the current device)
+  bool stream_k;      // split the final partial wave by K iterations
+  int* flags;         // stream-K fix-up flags: >= flags_cap zeroed ints, private to the stream
+  int flags_cap;
 };
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).

@@ -29,6 +29,7 @@ static int cuda_fail(cudaError_t e, const char* what) {
 // Device copies of a plan's tables on one device.
 struct DeviceTables {
   int device = -1;
+  int num_sms = 148;
   void* tab[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint8_t* vA = nullptr;
   uint8_t* vB = nullptr;
@@ -42,6 +43,31 @@ struct DeviceTables {
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
+
+// Stream-K fix-up flags, one zeroed buffer of 2 * #SMs ints per (device, stream). The kernel
+// leaves every flag at 0 when it ends, so a buffer is reused without a reset; launches on one
+// stream are ordered, launches on different streams use different buffers.
+struct FlagKey {
+  int device;
+  cudaStream_t stream;
+  bool operator<(const FlagKey& o) const {
+    return device != o.device ? device < o.device : stream < o.stream;
+  }
+};
+static std::mutex g_flags_mu;
+static std::map<FlagKey, int*> g_flags;
+
+static int* stream_flags(int device, cudaStream_t s, int cap) {
+  std::lock_guard<std::mutex> lk(g_flags_mu);
+  auto it = g_flags.find({device, s});
+  if (it != g_flags.end()) return it->second;
+  int* f = nullptr;
+  if (cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int) * (size_t)cap) != cudaSuccess)
+    return nullptr;
+  if (cudaMemset(f, 0, sizeof(int) * (size_t)cap) != cudaSuccess) { cudaFree(f); return nullptr; }
+  g_flags[{device, s}] = f;
+  return f;
+}
 
 Plan::~Plan() {
   for (auto* d : dev) delete d;
@@ -86,6 +112,7 @@ static int get_tables(const Plan& p, DeviceTables** out) {
     if (d->device == dev) { *out = d; return TC_OK; }
   auto* d = new DeviceTables();
   d->device = dev;
+  cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, dev);
   for (int i = 0; i < 6; ++i) {
     e = p.idx64 ? upload_table<long long>(p.scat[i], &d->tab[i])
                 : upload_table<int>(p.scat[i], &d->tab[i]);
@@ -128,6 +155,10 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
   a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0;
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0;
+  a.num_sms = d->num_sms;
+  a.flags_cap = 2 * d->num_sms;
+  a.flags = stream_flags(d->device, stream, a.flags_cap);
+  a.stream_k = a.flags != nullptr;
   if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
   int n = launch_contract(a, stream);
   if (n < 0) return cuda_fail(cudaGetLastError(), "kernel launch");

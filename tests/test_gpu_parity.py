@@ -356,3 +356,35 @@ def test_f32_misaligned_views():
         tc().contract("mn-mk-kn", bigA.cuda()[off:off + 65, 3, :57],
                       bigB.cuda()[:57, 2, off:off + 47], Cd, 1.0, -1.0)
         assert relerr(Cd.cpu().numpy(), ref.numpy()) < 1e-6
+
+
+# ---------------------------------------------------------------------------------------------
+# persistent schedule: data-parallel waves + stream-K tail
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("mnk", [(100, 120, 20000), (128, 128, 4096), (1000, 1200, 700),
+                                 (128 * 12, 128 * 13, 2000), (2048, 2048, 64)])
+@pytest.mark.parametrize("beta", [0.0, 0.75])
+def test_stream_k_splits(mnk, beta):
+    """Single tiles with long K (up to 16 pieces per tile), partial waves, 156 tiles (one wave
+    plus 8), and a short K; beta != 0 exercises the ordered fix-up of the first piece."""
+    case = W.Case("sk", "mn", "mk", "kn", dict(zip("mnk", mnk)), alpha=0.5, beta=beta,
+                  c_init="dist", seed=31)
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
+def test_stream_k_deterministic_and_matches_data_parallel():
+    case = W.Case("skd", "mn", "mk", "kn", {"m": 1900, "n": 1700, "k": 3000}, alpha=1.0,
+                  beta=0.5, c_init="dist", seed=32)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    outs = []
+    for _ in range(3):
+        C = Cd.clone()
+        tc().contract(case.spec, Ad, Bd, C, case.alpha, case.beta)
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = case.alpha * (Ad @ Bd) + case.beta * Cd
+    assert relerr(outs[0].cpu().numpy(), ref.cpu().numpy()) < 1e-12
