@@ -1,5 +1,7 @@
 // C ABI (include/tc.h): validation, plan cache, device tables, host (end-to-end) path.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -103,6 +105,17 @@ static cudaError_t upload_bytes(const std::vector<uint8_t>& v, uint8_t** out) {
   return cudaMemcpy(*out, v.data(), v.size(), cudaMemcpyHostToDevice);
 }
 
+// TC_FORCE_PATH=scatter: ablation of the block-scatter fast paths (the paper's SMTC):
+// every vector flag is 0 and no operand is treated as vectorisable, so every element is an
+// individual gather through the scatter vectors.
+static bool force_scatter() {
+  static const bool f = [] {
+    const char* e = getenv("TC_FORCE_PATH");
+    return e && !strcmp(e, "scatter");
+  }();
+  return f;
+}
+
 static int get_tables(const Plan& p, DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -122,8 +135,14 @@ static int get_tables(const Plan& p, DeviceTables** out) {
   const std::vector<int64_t>& ta = p.a_vec_m ? p.scat[0] : p.scat[1];
   const std::vector<int64_t>& tb = p.b_vec_k ? p.scat[2] : p.scat[3];
   const int64_t V = p.dtype == TC_F64 ? 2 : 4;
-  e = upload_bytes(vec_flags(ta, padded((int64_t)ta.size()), V), &d->vA);
-  if (e == cudaSuccess) e = upload_bytes(vec_flags(tb, padded((int64_t)tb.size()), V), &d->vB);
+  std::vector<uint8_t> fa = vec_flags(ta, padded((int64_t)ta.size()), V);
+  std::vector<uint8_t> fb = vec_flags(tb, padded((int64_t)tb.size()), V);
+  if (force_scatter()) {
+    std::fill(fa.begin(), fa.end(), 0);
+    std::fill(fb.begin(), fb.end(), 0);
+  }
+  e = upload_bytes(fa, &d->vA);
+  if (e == cudaSuccess) e = upload_bytes(fb, &d->vB);
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "flag upload"); }
   p.dev.push_back(d);
   *out = d;
@@ -153,8 +172,8 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.M = (int)p.m; a.N = (int)p.n; a.K = skip_ab ? 0 : (int)p.k;
   a.alpha = alpha; a.beta = beta;
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
-  a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0;
-  a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0;
+  a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0 && !force_scatter();
+  a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !force_scatter();
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;
   a.flags = stream_flags(d->device, stream, a.flags_cap);

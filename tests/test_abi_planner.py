@@ -142,3 +142,14 @@ def test_planner_rank_limit():
         tc.Plan(f"{labs}-{labs[:9]}-{labs[9:]}", torch.float64,
                 ([1] * 9, [1] * 8, [1] * 17), ([1] * 9, [1] * 8, [1] * 17))
     assert e.value.code in (2, 5)
+
+
+@pytest.mark.parametrize("idx", range(24))
+def test_planner_fig_bench_structures(idx):
+    """The paper's 24 fig:bench index strings at small synthetic sizes."""
+    _compare(W.fig_bench(idx, elems=2 ** 10))
+
+
+@pytest.mark.parametrize("i", range(7))
+def test_planner_rankk_structures(i):
+    _compare(W.rankk(i, mn=60))

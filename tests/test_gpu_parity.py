@@ -388,3 +388,45 @@ def test_stream_k_deterministic_and_matches_data_parallel():
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     ref = case.alpha * (Ad @ Bd) + case.beta * Cd
     assert relerr(outs[0].cpu().numpy(), ref.cpu().numpy()) < 1e-12
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) follow-on families: f2 = the paper's 24 fig:bench index strings (synthetic sizes),
+# f1 = rank-k updates (m = n = 16000, k = 5..500)
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("idx", range(24))
+def test_f2_fig_bench_scaled_full(idx):
+    case = W.fig_bench(idx, elems=2 ** 12)
+    case.c_init, case.beta = "dist", -0.5
+    check(case)
+
+
+@pytest.mark.parametrize("idx", range(24))
+def test_f2_fig_bench_full_sampled(idx):
+    case = W.fig_bench(idx)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=2, seed=idx)
+    assert torch.isfinite(c1).all()
+    assert e < 1e-12
+
+
+@pytest.mark.parametrize("i", range(7))
+def test_f1_rankk_full_sampled(i):
+    case = W.rankk(i)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=3, seed=i)
+    assert torch.isfinite(c1).all()
+    assert e < 1e-12
+    del Ad, Bd, Cd, C0
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("i", range(7))
+def test_f1_rankk_scaled_full(i):
+    case = W.rankk(i, mn=300)
+    check(case)

@@ -55,10 +55,15 @@ def ttdt(case, A, B, C):
     return run
 
 
-def cases(only):
-    out = [W.cfg1(), W.cfg2(False), W.cfg2(True), W.cfg3(False), W.cfg3(True)]
-    out += [W.cfg4(i) for i in range(20)] + [W.cfg4(i, torch.float32) for i in range(20)]
-    out.append(W.cfg5())
+def cases(only, family):
+    if family == "f2":
+        out = [W.fig_bench(i) for i in range(24)]
+    elif family == "f1":
+        out = [W.rankk(i) for i in range(7)]
+    else:
+        out = [W.cfg1(), W.cfg2(False), W.cfg2(True), W.cfg3(False), W.cfg3(True)]
+        out += [W.cfg4(i) for i in range(20)] + [W.cfg4(i, torch.float32) for i in range(20)]
+        out.append(W.cfg5())
     return [c for c in out if not only or c.name.startswith(only)]
 
 
@@ -67,8 +72,9 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-ttdt", action="store_true")
+    ap.add_argument("--family", default="baseline", choices=["baseline", "f1", "f2"])
     args = ap.parse_args()
-    for case in cases(args.only):
+    for case in cases(args.only, args.family):
         A, B, C = W.make_tensors(case, "cuda")
         if case.c_init == "nan":
             C.zero_()
@@ -87,7 +93,11 @@ def main():
                "swapped": info["swapped"], "a_vec_m": info["a_vec_m"], "b_vec_k": info["b_vec_k"],
                "ms": round(t, 4), "gflops": round(fl / t / 1e6, 1),
                "gemm_ms": round(tg, 4), "gemm_gflops": round(fl / tg / 1e6, 1),
-               "vs_gemm": round(tg / t, 3)}
+               "vs_gemm": round(tg / t, 3),
+               # compulsory HBM traffic (A, B read once, C written, read too when beta != 0)
+               "hbm_gbs": round(A.element_size() * (A.numel() + B.numel() + C.numel() *
+                                                     (2 if case.beta != 0 else 1)) / t / 1e6, 1),
+               "force_path": os.environ.get("TC_FORCE_PATH", "")}
         if not args.no_ttdt and fl < 2e12:
             try:
                 tt = timeit(ttdt(case, A, B, C.clone()), reps)

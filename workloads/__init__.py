@@ -229,3 +229,62 @@ def random_tiny_case(seed: int, max_rank: int = 6, max_len: int = 5, dist: str =
     return Case(f"tiny_{seed}", perm(li + lj), perm(li + lp), perm(lp + lj), lens, dtype=dtype,
                 dist=dist, alpha=ab[int(rs.randint(1, 4))], beta=ab[int(rs.randint(0, 4))],
                 c_init="dist", seed=SEED_BASE + 900000 + seed)
+
+
+# ---------------------------------------------------------------------------------------------
+# §8(f) follow-on families
+# ---------------------------------------------------------------------------------------------
+
+def fig_bench(idx: int, elems: int = 2 ** 25, dtype: torch.dtype = torch.float64) -> Case:
+    """f2: entry `idx` of the paper's fig:bench (C-A-B order P:1327-1329) with synthetic
+    sizes (the paper does not give them): every index has the same length
+    L = round(elems ** (1 / r_max)), r_max the largest operand rank, so the largest operand holds
+    about `elems` elements. Contractions whose bound bundle is a single short index stay
+    bandwidth-bound and GEMM-like ones compute-bound, as in the paper's left-to-right order."""
+    spec = FIG_BENCH_SPECS[idx]
+    lab_c, lab_a, lab_b = spec.split("-")
+    r_max = max(len(lab_a), len(lab_b), len(lab_c))
+    L = int(round(elems ** (1.0 / r_max)))
+    lens = {x: L for x in set(lab_a + lab_b + lab_c)}
+    return Case(f"f2_{idx:02d}_{spec}", lab_c, lab_a, lab_b, lens, dtype=dtype, dist="uniform",
+                alpha=1.0, beta=0.0, c_init="nan", seed=SEED_BASE + 600 + idx)
+
+
+RANKK_K = [5, 16, 32, 64, 128, 256, 500]
+
+
+def _factor(rs: np.random.RandomState, g: int, target: int) -> List[int]:
+    if g == 1:
+        return [int(target)]
+    for _ in range(100000):
+        base = target ** (1.0 / g)
+        first = [max(2, int(round(base * rs.uniform(0.8, 1.25)))) for _ in range(g - 1)]
+        last = max(2, int(round(target / math.prod(first))))
+        lens = first + [last]
+        if 0.75 * target <= math.prod(lens) <= 1.25 * target:
+            rs.shuffle(lens)
+            return lens
+    raise RuntimeError("factor draw failed")
+
+
+def rankk(i: int, mn: int = 16000, dtype: torch.dtype = torch.float64) -> Case:
+    """f1: rank-k update family: m = n = 16000 (the paper's 12-core size),
+    k = RANKK_K[i % 7] (5-500), each bundle split into 1-3 indices with product within +-25%
+    of its target (bound bundles with k < 64 keep one index), operand index orders randomly
+    permuted (P:1159-1165). alpha = 1, beta = 0."""
+    k = RANKK_K[i % len(RANKK_K)]
+    rs = np.random.RandomState(SEED_BASE + 700 + i)
+    gm, gn = int(rs.randint(1, 4)), int(rs.randint(1, 4))
+    gk = 1 if k < 64 else int(rs.randint(1, 3))
+    pool = list("abcdefghijklmnopqr")
+    rs.shuffle(pool)
+    li, lj, lp = pool[:gm], pool[gm:gm + gn], pool[gm + gn:gm + gn + gk]
+    lens = {}
+    for labs, t in ((li, mn), (lj, mn), (lp, k)):
+        for x, n in zip(labs, _factor(rs, len(labs), t)):
+            lens[x] = n
+    perm = lambda labs: "".join(rs.permutation(labs))  # noqa: E731
+    lab_a, lab_b, lab_c = perm(li + lp), perm(lp + lj), perm(li + lj)
+    return Case(f"f1_k{k}_{i:02d}_{lab_c}-{lab_a}-{lab_b}", lab_c, lab_a, lab_b, lens,
+                dtype=dtype, dist="uniform", alpha=1.0, beta=0.0, c_init="nan",
+                seed=SEED_BASE + 700 + i)
