@@ -1,6 +1,10 @@
-"""Build libtc_b200.so in-tree with nvcc for sm_100a (called by __graft_entry__.build())."""
+"""Build libtc_b200.so in-tree with nvcc for sm_100a (called by __graft_entry__.build()).
+
+Each translation unit is compiled to an object in parallel (the kernel instantiations are split
+over ws_*.cu), then linked into one shared library."""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -9,8 +13,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtc_b200.so")
-SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "contract_ws.cu"]
-HEADERS = ["plan.hpp", "kernels.hpp", "dev_common.cuh"]
+OBJ = os.path.join(HERE, "build_obj")
+SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "ws_f64.cu", "ws_f32_ffma.cu",
+           "ws_f32_dmma.cu"]
+HEADERS = ["plan.hpp", "kernels.hpp", "dev_common.cuh", "contract_ws.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -19,29 +25,52 @@ NVCC_FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
+def _deps_mtime() -> float:
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "tc.h")]
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return max(os.path.getmtime(d) for d in deps if os.path.exists(d))
+
+
+def _stale() -> bool:
+    return not os.path.exists(LIB) or os.path.getmtime(LIB) < _deps_mtime()
+
+
+def _compile(nvcc: str, src: str):
+    obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
+           os.path.join(CSRC, src), "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    return src, obj, cmd, res
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    os.makedirs(OBJ, exist_ok=True)
+    log = []
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(lambda s: _compile(nvcc, s), SOURCES))
+    failed = False
+    for src, obj, cmd, res in results:
+        log.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        if res.returncode != 0:
+            failed = True
+            sys.stderr.write(res.stderr[-6000:])
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [nvcc, *NVCC_FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", tmp, "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    if not failed:
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+               *[r[1] for r in results], "-o", tmp, "-lcudart"]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        log.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        failed = res.returncode != 0
+        if failed:
+            sys.stderr.write(res.stderr[-6000:])
     with open(os.path.join(HERE, "build.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stderr[-8000:])
+        f.write("\n".join(log))
+    if failed:
         raise RuntimeError("nvcc build of libtc_b200.so failed (see paper_1607_00291_b200/build.log)")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("\n".join(log))
     os.replace(tmp, LIB)
     return LIB
 

@@ -322,7 +322,14 @@ int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-int launch_ws(const LaunchArgs& a, cudaStream_t stream);   // contract_ws.cu
+int launch_ws_f64(const LaunchArgs& a, cudaStream_t stream);        // ws_f64.cu
+int launch_ws_f32_ffma(const LaunchArgs& a, cudaStream_t stream);   // ws_f32_ffma.cu
+int launch_ws_f32_dmma(const LaunchArgs& a, cudaStream_t stream);   // ws_f32_dmma.cu
+
+static int launch_ws(const LaunchArgs& a, cudaStream_t stream) {
+  if (!a.f32) return launch_ws_f64(a, stream);
+  return a.f32_dmma ? launch_ws_f32_dmma(a, stream) : launch_ws_f32_ffma(a, stream);
+}
 
 // Kernel selection: the warp-specialised kernel (contract_ws.cu, fp64 and fp32) is the default;
 // TC_KERNEL=simple selects the first (non-specialised, fp64-only) kernel for ablation.

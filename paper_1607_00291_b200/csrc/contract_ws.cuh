@@ -1,4 +1,5 @@
-// Warp-specialised sm_100a contraction kernel (the production path).
+#pragma once
+// Warp-specialised sm_100a contraction kernel (templates; instantiated by ws_*.cu) (the production path).
 //
 //   warps 8-11  producers: gather the A and B tiles of each K step from global memory into a
 //               STAGES-deep shared-memory ring with cp.async ("packing", PAPER.md P:593-603,
@@ -75,6 +76,27 @@ template <typename T> __device__ __forceinline__ void cp_async_elem(T* d, const 
 // VEC: every vector is contiguous and 16-byte aligned (plan-time check), so each slot is one
 // 16-byte cp.async with zero-fill outside the extents.
 // ------------------------------------------------------------------------------------------
+// One vector of 16/sizeof(T) consecutive elements whose start may not be 16-byte aligned (the
+// smem destination always is): one 16-byte copy when aligned, else the widest copies whose
+// source and destination are both aligned.
+template <typename T>
+__device__ __forceinline__ void copy_contig(T* d, const T* p) {
+  if (aligned16(p)) {
+    cp_async16(d, p, true);
+  } else if constexpr (sizeof(T) == 4) {
+    if ((reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+      cp_async8(d, p, true);
+      cp_async8(d + 2, p + 2, true);
+    } else {   // source and destination 8-byte alignments differ: element copies
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cp_async4(d + j, p + j, true);
+    }
+  } else {
+    cp_async8(d, p, true);
+    cp_async8(d + 1, p + 1, true);
+  }
+}
+
 template <typename T, typename IDX, bool FIXED_VECS, bool VEC, int LD>
 struct Gather {
   static constexpr int V = 16 / sizeof(T);
@@ -127,8 +149,8 @@ struct Gather {
         if constexpr (VEC) {
           cp_async16(d, p0, kin && (vm & 1u));
         } else {
-          if (((vm >> V) & 1u) && kin && aligned16(p0)) {
-            cp_async16(d, p0, true);
+          if (((vm >> V) & 1u) && kin) {
+            copy_contig(d, p0);
           } else {
 #pragma unroll
             for (int j = 0; j < V; ++j)
@@ -159,8 +181,8 @@ struct Gather {
           const bool rin = (rv >> i) & 1u;
           T* d = d0 + r * LD;
           const T* p0 = g + (ro[i] + c[0]);
-          if (kvec && rin && aligned16(p0)) {
-            cp_async16(d, p0, true);
+          if (kvec && rin) {
+            copy_contig(d, p0);
           } else {
 #pragma unroll
             for (int j = 0; j < V; ++j)
@@ -170,6 +192,196 @@ struct Gather {
       }
     }
   }
+};
+
+// ------------------------------------------------------------------------------------------
+// Micro-kernels (register-tiled C += A.B over one K step). Each thread owns
+// an 8 x 8 block of its warp's 64 x 32 tile, exposed as acc[r][c] at (row(r), col(c)), so the
+// epilogue is shared.
+//  MicroDmma: mma.sync m16n8k4 f64 (DMMA.8x8x4) with fp64 accumulators; fp32 operands are
+//             widened on the shared-memory load (fp64 accumulation, one rounding at the end).
+//  MicroFfma: fp32 FFMA outer products with fp32 accumulators (the FMA micro-kernel of the
+//             north star for fp32): 16-byte shared loads along each layout's contiguous
+//             direction, 64 FFMA per 16 loaded values.
+// ------------------------------------------------------------------------------------------
+template <typename T, bool A_VM, bool B_VK>
+struct MicroDmma {
+  using Acc = double;
+  using AL = ALay<T, A_VM>;
+  using BL = BLay<T, B_VK>;
+  Acc acc[8][8];      // row r = 2i+h: m = wm + 16i + g + 8h; col c = 2j+e: n = wn + 8j + 2t + e
+  int wm, wn, g, t;
+  __device__ __forceinline__ void setup(int warp, int lane) {
+    g = lane >> 2; t = lane & 3; wm = (warp & 1) * WM; wn = (warp >> 1) * WN;
+  }
+  __device__ __forceinline__ int row(int r) const { return wm + 16 * (r >> 1) + g + 8 * (r & 1); }
+  __device__ __forceinline__ int col(int c) const { return wn + 8 * (c >> 1) + 2 * t + (c & 1); }
+  __device__ __forceinline__ double value(int r, int c) const { return acc[r][c]; }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
+  }
+  __device__ __forceinline__ void stage(const T* as, const T* bs) {
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[4][2], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i][0] = static_cast<double>(as[AL::at(wm + 16 * i + g, 4 * kk + t)]);
+        a[i][1] = static_cast<double>(as[AL::at(wm + 16 * i + g + 8, 4 * kk + t)]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        b[j] = static_cast<double>(bs[BL::at(4 * kk + t, wn + 8 * j + g)]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dmma16x8x4(acc[2 * i][2 * j], acc[2 * i][2 * j + 1], acc[2 * i + 1][2 * j],
+                     acc[2 * i + 1][2 * j + 1], a[i][0], a[i][1], b[j]);
+    }
+  }
+};
+
+// d0 += a0 * b0, d1 += a1 * b1 as one packed fp32x2 FMA (SASS FFMA2; a0 == a1 becomes the
+// scalar-broadcast form). Two FMAs per lane per issue slot.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0,
+                                      float b1) {
+  unsigned long long d, x, y;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(d) : "f"(d0), "f"(d1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(x) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(y) : "f"(b0), "f"(b1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(x), "l"(y));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+
+template <bool A_VM, bool B_VK>
+struct MicroFfma {
+  using Acc = float;
+  using AL = ALay<float, A_VM>;
+  using BL = BLay<float, B_VK>;
+  // FFMA2 pairs two accumulators whose operands sit in adjacent registers of a 16-byte load:
+  //  PAIR_C: (acc[r][c], acc[r][c+1]) with b[k][c..c+1] from one load ([k][n] layout of B)
+  //  PAIR_R: (acc[r][c], acc[r+1][c]) with a[k][r..r+1] ([k][m] layout of A, B is [n][k])
+  //  PAIR_K: (acc[r][c], acc2[r][c]) = even / odd k partial sums ([m][k] and [n][k] layouts)
+  static constexpr int PAIR_C = 0, PAIR_R = 1, PAIR_K = 2;
+  static constexpr int MODE = !B_VK ? PAIR_C : (A_VM ? PAIR_R : PAIR_K);
+  Acc acc[8][8];
+  Acc acc2[MODE == PAIR_K ? 8 : 1][MODE == PAIR_K ? 8 : 1];
+  int wm, wn, tm, tn;     // lane = tm + 8 tn (tm 0..7 over M, tn 0..3 over N)
+  __device__ __forceinline__ void setup(int warp, int lane) {
+    tm = lane & 7; tn = lane >> 3; wm = (warp & 1) * WM; wn = (warp >> 1) * WN;
+  }
+  // [k][m] rows: two runs of 4 consecutive m (16-byte loads); [m][k]: rows tm + 8r (a 16-byte
+  // load gives 4 consecutive k). Same for columns of B ([k][n] runs / [n][k] rows tn + 4c).
+  __device__ __forceinline__ int row(int r) const {
+    return A_VM ? wm + (r < 4 ? 4 * tm + r : 32 + 4 * tm + r - 4) : wm + tm + 8 * r;
+  }
+  __device__ __forceinline__ int col(int c) const {
+    return !B_VK ? wn + (c < 4 ? 4 * tn + c : 16 + 4 * tn + c - 4) : wn + tn + 4 * c;
+  }
+  __device__ __forceinline__ float value(int r, int c) const {
+    if constexpr (MODE == PAIR_K) return acc[r][c] + acc2[r][c];
+    else return acc[r][c];
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[r][c] = 0.f;
+    if constexpr (MODE == PAIR_K) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc2[r][c] = 0.f;
+    }
+  }
+  __device__ __forceinline__ void stage(const float* as, const float* bs) {
+    if constexpr (MODE == PAIR_K) {
+      // [m][k] x [n][k]: 8-byte loads of 2 consecutive k keep the fragments at 32 registers
+      // next to the two 64-float accumulator sets
+#pragma unroll 2
+      for (int k2 = 0; k2 < BK / 2; ++k2) {
+        float a[2][8], b[2][8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float2 x = *reinterpret_cast<const float2*>(as + (wm + tm + 8 * r) * AL::LD + 2 * k2);
+          a[0][r] = x.x; a[1][r] = x.y;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float2 x = *reinterpret_cast<const float2*>(bs + (wn + tn + 4 * c) * BL::LD + 2 * k2);
+          b[0][c] = x.x; b[1][c] = x.y;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            ffma2(acc[r][c], acc2[r][c], a[0][r], a[1][r], b[0][c], b[1][c]);
+      }
+      return;
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      float a[4][8], b[4][8];
+      if constexpr (A_VM) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 x = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 4 * tm);
+          const float4 y = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 32 + 4 * tm);
+          a[k][0] = x.x; a[k][1] = x.y; a[k][2] = x.z; a[k][3] = x.w;
+          a[k][4] = y.x; a[k][5] = y.y; a[k][6] = y.z; a[k][7] = y.w;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const float4 x = *reinterpret_cast<const float4*>(as + (wm + tm + 8 * r) * AL::LD + 4 * kk);
+          a[0][r] = x.x; a[1][r] = x.y; a[2][r] = x.z; a[3][r] = x.w;
+        }
+      }
+      if constexpr (!B_VK) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float4 x = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 4 * tn);
+          const float4 y = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 16 + 4 * tn);
+          b[k][0] = x.x; b[k][1] = x.y; b[k][2] = x.z; b[k][3] = x.w;
+          b[k][4] = y.x; b[k][5] = y.y; b[k][6] = y.z; b[k][7] = y.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = *reinterpret_cast<const float4*>(bs + (wn + tn + 4 * c) * BL::LD + 4 * kk);
+          b[0][c] = x.x; b[1][c] = x.y; b[2][c] = x.z; b[3][c] = x.w;
+        }
+      }
+      if constexpr (MODE == PAIR_C) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; c += 2)
+              ffma2(acc[r][c], acc[r][c + 1], a[k][r], a[k][r], b[k][c], b[k][c + 1]);
+      } else {   // PAIR_R
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int r = 0; r < 8; r += 2)
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              ffma2(acc[r][c], acc[r + 1][c], a[k][r], a[k][r + 1], b[k][c], b[k][c]);
+      }
+    }
+  }
+};
+
+template <typename T, bool FFMA, bool A_VM, bool B_VK> struct MicroSel {
+  using type = MicroDmma<T, A_VM, B_VK>;
+};
+template <bool A_VM, bool B_VK> struct MicroSel<float, true, A_VM, B_VK> {
+  using type = MicroFfma<A_VM, B_VK>;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -232,7 +444,7 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
 }
 
-template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC>
+template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC, bool FFMA>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                   const IDX* __restrict__ rA, const IDX* __restrict__ cA,
@@ -294,8 +506,8 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
 
   // --------------------------------- consumers ---------------------------------
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 1) * WM, wn = (warp >> 1) * WN;
+  typename MicroSel<T, FFMA, A_VM, B_VK>::type mk;
+  mk.setup(warp, lane);
   while (wi.next(tile, kb, ke, sk)) {
     int tm, tn;
     tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
@@ -303,45 +515,21 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     if (beta != 0.0 && kb == 0 && ke - kb >= 4) {
       // pull the warp's 64 x 32 block of C into L2 while the K loop runs: lane l takes column
       // l and four 16-row runs (one 128-byte line each when C is contiguous along M)
-      const int n = n0 + wn + lane;
+      const int n = n0 + (warp >> 1) * WN + lane;
       if (n < N) {
         const IDX c = cC[n];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int m = m0 + wm + 16 * q;
+          const int m = m0 + (warp & 1) * WM + 16 * q;
           if (m < M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + (rC[m] + c)));
         }
       }
     }
-    double acc[4][4][4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
-
+    mk.zero();
     for (int kt = kb; kt < ke; ++kt, ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
-      const T* as = As + s * AL::STAGE;
-      const T* bs = Bs + s * BL::STAGE;
-#pragma unroll
-      for (int kk = 0; kk < BK / 4; ++kk) {
-        double a[4][2], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          a[i][0] = static_cast<double>(as[AL::at(wm + 16 * i + g, 4 * kk + t)]);
-          a[i][1] = static_cast<double>(as[AL::at(wm + 16 * i + g + 8, 4 * kk + t)]);
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          b[j] = static_cast<double>(bs[BL::at(4 * kk + t, wn + 8 * j + g)]);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
-      }
+      mk.stage(As + s * AL::STAGE, Bs + s * BL::STAGE);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -366,56 +554,49 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     const bool accumulate = split && piece > 0;
 
     // epilogue: C[rC[m] + cC[n]] = alpha*acc + beta*C (beta == 0: C not read); computed in
-    // fp64, rounded once to T. C is read in chunks of 16 independent loads (one m16 row block)
-    // so the loads of a chunk overlap instead of each waiting behind the previous store.
+    // fp64, rounded once to T. C is read in chunks of 16 independent loads (two of the thread's
+    // rows) so the loads of a chunk overlap instead of each waiting behind the previous store.
     IDX cc[8];
     int nn[8];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = n0 + wn + 8 * j + 2 * t + e;
-        nn[2 * j + e] = n;
-        cc[2 * j + e] = cC[n];
-      }
+    for (int c = 0; c < 8; ++c) {
+      nn[c] = n0 + mk.col(c);
+      cc[c] = cC[nn[c]];
+    }
     const bool read_c = accumulate || beta != 0.0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int r2 = 0; r2 < 4; ++r2) {
       int mm[2];
       IDX rc[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        mm[h] = m0 + wm + 16 * i + g + 8 * h;
+        mm[h] = m0 + mk.row(2 * r2 + h);
         rc[h] = rC[mm[h]];
       }
-      double old[2][4][2];
+      double old[2][8];
       if (read_c) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              old[h][j][e] = 0.0;
-              if (mm[h] < M && nn[2 * j + e] < N) {
-                const T* q = C + (rc[h] + cc[2 * j + e]);
-                old[h][j][e] = static_cast<double>(accumulate ? __ldcg(q) : *q);
-              }
+          for (int c = 0; c < 8; ++c) {
+            old[h][c] = 0.0;
+            if (mm[h] < M && nn[c] < N) {
+              const T* q = C + (rc[h] + cc[c]);
+              old[h][c] = static_cast<double>(accumulate ? __ldcg(q) : *q);
             }
+          }
       }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         if (mm[h] >= M) continue;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            if (nn[2 * j + e] >= N) continue;
-            double v = alpha * acc[i][j][2 * h + e];
-            if (accumulate) v += old[h][j][e];
-            else if (beta != 0.0) v = fma(beta, old[h][j][e], v);
-            C[rc[h] + cc[2 * j + e]] = static_cast<T>(v);
-          }
+        for (int c = 0; c < 8; ++c) {
+          if (nn[c] >= N) continue;
+          double v = alpha * static_cast<double>(mk.value(2 * r2 + h, c));
+          if (accumulate) v += old[h][c];
+          else if (beta != 0.0) v = fma(beta, old[h][c], v);
+          C[rc[h] + cc[c]] = static_cast<T>(v);
+        }
       }
     }
     if (split) {
@@ -453,12 +634,12 @@ static Sched make_sched(int T, int KT, int nsm, bool allow_sk) {
   return s;
 }
 
-template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC>
+template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC, bool FFMA>
 int launch(const LaunchArgs& a, cudaStream_t stream) {
   constexpr int smem =
       ((STAGES * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) * (int)sizeof(T) + 15) / 16) * 16 +
       2 * STAGES * (int)sizeof(uint64_t);
-  auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_VEC, B_VEC>;
+  auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_VEC, B_VEC, FFMA>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -485,29 +666,24 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   return 1;
 }
 
-template <typename T, typename IDX, bool A_VEC, bool B_VEC>
+template <typename T, typename IDX, bool A_VEC, bool B_VEC, bool FFMA>
 int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
   if (a.a_vec_m)
-    return a.b_vec_k ? launch<T, IDX, true, true, A_VEC, B_VEC>(a, s)
-                     : launch<T, IDX, true, false, A_VEC, B_VEC>(a, s);
-  return a.b_vec_k ? launch<T, IDX, false, true, A_VEC, B_VEC>(a, s)
-                   : launch<T, IDX, false, false, A_VEC, B_VEC>(a, s);
+    return a.b_vec_k ? launch<T, IDX, true, true, A_VEC, B_VEC, FFMA>(a, s)
+                     : launch<T, IDX, true, false, A_VEC, B_VEC, FFMA>(a, s);
+  return a.b_vec_k ? launch<T, IDX, false, true, A_VEC, B_VEC, FFMA>(a, s)
+                   : launch<T, IDX, false, false, A_VEC, B_VEC, FFMA>(a, s);
 }
 
-template <typename T>
+template <typename T, bool FFMA>
 int dispatch_type(const LaunchArgs& a, cudaStream_t stream) {
-  if (a.idx64) return dispatch_dir<T, long long, false, false>(a, stream);
+  if (a.idx64) return dispatch_dir<T, long long, false, false, FFMA>(a, stream);
   if (a.a_vec_all)
-    return a.b_vec_all ? dispatch_dir<T, int, true, true>(a, stream)
-                       : dispatch_dir<T, int, true, false>(a, stream);
-  return a.b_vec_all ? dispatch_dir<T, int, false, true>(a, stream)
-                     : dispatch_dir<T, int, false, false>(a, stream);
+    return a.b_vec_all ? dispatch_dir<T, int, true, true, FFMA>(a, stream)
+                       : dispatch_dir<T, int, true, false, FFMA>(a, stream);
+  return a.b_vec_all ? dispatch_dir<T, int, false, true, FFMA>(a, stream)
+                     : dispatch_dir<T, int, false, false, FFMA>(a, stream);
 }
 
 }  // namespace ws
-
-int launch_ws(const LaunchArgs& a, cudaStream_t stream) {
-  return a.f32 ? ws::dispatch_type<float>(a, stream) : ws::dispatch_type<double>(a, stream);
-}
-
 }  // namespace tcb

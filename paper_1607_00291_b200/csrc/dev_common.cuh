@@ -77,6 +77,15 @@ __device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1,
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
+__device__ __forceinline__ void dmma16x8x4(double& d0, double& d1, double& d2, double& d3,
+                                           double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d0), "+d"(d1), "+d"(d2), "+d"(d3)
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
 // Tile rasterisation: GROUP_M consecutive M-tiles walk the N-tiles together so that CTAs
 // running at the same time share A and B panels in L2.
 template <int GROUP_M>

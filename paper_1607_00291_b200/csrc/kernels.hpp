@@ -31,6 +31,7 @@ struct LaunchArgs {
   bool a_vec_all, b_vec_all;
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
+  bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA
   int* flags;         // stream-K fix-up flags: >= flags_cap zeroed ints, private to the stream
   int flags_cap;
 };

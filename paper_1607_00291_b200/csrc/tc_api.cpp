@@ -116,6 +116,16 @@ static bool force_scatter() {
   return f;
 }
 
+// TC_F32_MMA=dmma: fp32 contractions through the DMMA micro-kernel (fp64 accumulation, one
+// rounding) instead of the default FFMA micro-kernel (fp32 accumulation).
+static bool f32_dmma() {
+  static const bool f = [] {
+    const char* e = getenv("TC_F32_MMA");
+    return e && !strcmp(e, "dmma");
+  }();
+  return f;
+}
+
 static int get_tables(const Plan& p, DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -178,6 +188,7 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.flags_cap = 2 * d->num_sms;
   a.flags = stream_flags(d->device, stream, a.flags_cap);
   a.stream_k = a.flags != nullptr;
+  a.f32_dmma = f32_dmma();
   if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
   int n = launch_contract(a, stream);
   if (n < 0) return cuda_fail(cudaGetLastError(), "kernel launch");

@@ -430,3 +430,51 @@ def test_f1_rankk_full_sampled(i):
 def test_f1_rankk_scaled_full(i):
     case = W.rankk(i, mn=300)
     check(case)
+
+
+# ---------------------------------------------------------------------------------------------
+# guard bands (compute-sanitizer is closed on this pool): operands live inside NaN-filled
+# buffers, so reading any element outside an operand's index space poisons C; C lives inside a
+# sentinel-filled buffer whose untouched bytes must survive bitwise.
+# ---------------------------------------------------------------------------------------------
+
+def _embed(t, device, fill, rs, gap):
+    """Copy tensor t into a larger buffer (filled with `fill`) with random extra stride gaps and
+    a random offset; return the strided view."""
+    lens = list(t.shape)
+    order = list(rs.permutation(len(lens)))
+    strides, s = [0] * len(lens), 1
+    for d in order:
+        strides[d] = s
+        s *= lens[d] + int(rs.randint(0, gap + 1))
+    off = int(rs.randint(0, 5))
+    buf = torch.full((off + s + int(rs.randint(0, 9)),), fill, dtype=t.dtype, device=device)
+    view = buf.as_strided(lens, strides, off)
+    view.copy_(t.to(device))
+    return buf, view
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_guard_bands(seed, dtype):
+    rs = np.random.RandomState(1000 + seed)
+    case = W.random_tiny_case(seed, max_rank=6, max_len=9, dtype=dtype)
+    if seed % 3 == 0:   # a few larger ones: several tiles, stream-K pieces, ragged tails
+        case = W.cfg4(seed % 20, dtype)
+        case = case.scaled({x: max(2, min(n, int(round(n ** 0.55)))) for x, n in case.lens.items()})
+        case.beta, case.c_init = 0.5, "dist"
+    A, B, C = W.make_tensors(case, "cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    bufA, Ad = _embed(A, "cuda", float("nan"), rs, 3)
+    bufB, Bd = _embed(B, "cuda", float("nan"), rs, 3)
+    bufC, Cd = _embed(C, "cuda", 12345.0, rs, 3)
+    mask = torch.ones(bufC.numel(), dtype=torch.bool, device="cuda")
+    mask.as_strided(Cd.shape, Cd.stride(), Cd.storage_offset()).fill_(False)
+    before = bufC[mask].clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    assert torch.equal(bufC[mask], before), "write outside C"
+    got = Cd.cpu()
+    assert torch.isfinite(got).all() or not torch.isfinite(ref).all(), "read outside A/B"
+    assert relerr(got.numpy(), ref.numpy()) <= TOL[dtype]
