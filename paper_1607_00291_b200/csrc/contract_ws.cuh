@@ -298,80 +298,95 @@ struct MicroFfma {
         for (int c = 0; c < 8; ++c) acc2[r][c] = 0.f;
     }
   }
-  __device__ __forceinline__ void stage(const float* as, const float* bs) {
-    if constexpr (MODE == PAIR_K) {
-      // [m][k] x [n][k]: 8-byte loads of 2 consecutive k keep the fragments at 32 registers
-      // next to the two 64-float accumulator sets
-#pragma unroll 2
-      for (int k2 = 0; k2 < BK / 2; ++k2) {
-        float a[2][8], b[2][8];
+  // fragments of one group of 4 k (PAIR_C / PAIR_R) or 2 k (PAIR_K)
+  __device__ __forceinline__ void load4(const float* as, const float* bs, int kk, float (&a)[4][8],
+                                        float (&b)[4][8]) const {
+    if constexpr (A_VM) {
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const float2 x = *reinterpret_cast<const float2*>(as + (wm + tm + 8 * r) * AL::LD + 2 * k2);
-          a[0][r] = x.x; a[1][r] = x.y;
-        }
+      for (int k = 0; k < 4; ++k) {
+        const float4 x = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 4 * tm);
+        const float4 y = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 32 + 4 * tm);
+        a[k][0] = x.x; a[k][1] = x.y; a[k][2] = x.z; a[k][3] = x.w;
+        a[k][4] = y.x; a[k][5] = y.y; a[k][6] = y.z; a[k][7] = y.w;
+      }
+    } else {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float2 x = *reinterpret_cast<const float2*>(bs + (wn + tn + 4 * c) * BL::LD + 2 * k2);
-          b[0][c] = x.x; b[1][c] = x.y;
-        }
+      for (int r = 0; r < 8; ++r) {
+        const float4 x = *reinterpret_cast<const float4*>(as + (wm + tm + 8 * r) * AL::LD + 4 * kk);
+        a[0][r] = x.x; a[1][r] = x.y; a[2][r] = x.z; a[3][r] = x.w;
+      }
+    }
+    if constexpr (!B_VK) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float4 x = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 4 * tn);
+        const float4 y = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 16 + 4 * tn);
+        b[k][0] = x.x; b[k][1] = x.y; b[k][2] = x.z; b[k][3] = x.w;
+        b[k][4] = y.x; b[k][5] = y.y; b[k][6] = y.z; b[k][7] = y.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 x = *reinterpret_cast<const float4*>(bs + (wn + tn + 4 * c) * BL::LD + 4 * kk);
+        b[0][c] = x.x; b[1][c] = x.y; b[2][c] = x.z; b[3][c] = x.w;
+      }
+    }
+  }
+  __device__ __forceinline__ void load2(const float* as, const float* bs, int k2, float (&a)[2][8],
+                                        float (&b)[2][8]) const {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float2 x = *reinterpret_cast<const float2*>(as + (wm + tm + 8 * r) * AL::LD + 2 * k2);
+      a[0][r] = x.x; a[1][r] = x.y;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float2 x = *reinterpret_cast<const float2*>(bs + (wn + tn + 4 * c) * BL::LD + 2 * k2);
+      b[0][c] = x.x; b[1][c] = x.y;
+    }
+  }
+  __device__ __forceinline__ void fma4(const float (&a)[4][8], const float (&b)[4][8]) {
+    if constexpr (MODE == PAIR_C) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
+          for (int c = 0; c < 8; c += 2)
+            ffma2(acc[r][c], acc[r][c + 1], a[k][r], a[k][r], b[k][c], b[k][c + 1]);
+    } else {   // PAIR_R
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int r = 0; r < 8; r += 2)
+#pragma unroll
           for (int c = 0; c < 8; ++c)
-            ffma2(acc[r][c], acc2[r][c], a[0][r], a[1][r], b[0][c], b[1][c]);
-      }
-      return;
+            ffma2(acc[r][c], acc[r + 1][c], a[k][r], a[k][r + 1], b[k][c], b[k][c]);
     }
+  }
+  __device__ __forceinline__ void fma2k(const float (&a)[2][8], const float (&b)[2][8]) {
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      float a[4][8], b[4][8];
-      if constexpr (A_VM) {
+    for (int r = 0; r < 8; ++r)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 x = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 4 * tm);
-          const float4 y = *reinterpret_cast<const float4*>(as + (4 * kk + k) * AL::LD + wm + 32 + 4 * tm);
-          a[k][0] = x.x; a[k][1] = x.y; a[k][2] = x.z; a[k][3] = x.w;
-          a[k][4] = y.x; a[k][5] = y.y; a[k][6] = y.z; a[k][7] = y.w;
-        }
-      } else {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const float4 x = *reinterpret_cast<const float4*>(as + (wm + tm + 8 * r) * AL::LD + 4 * kk);
-          a[0][r] = x.x; a[1][r] = x.y; a[2][r] = x.z; a[3][r] = x.w;
-        }
+      for (int c = 0; c < 8; ++c)
+        ffma2(acc[r][c], acc2[r][c], a[0][r], a[1][r], b[0][c], b[1][c]);
+  }
+  // one K step: the fragments of the next k group load while the current one is consumed
+  __device__ __forceinline__ void stage(const float* as, const float* bs) {
+    if constexpr (MODE == PAIR_K) {
+#pragma unroll 2
+      for (int k2 = 0; k2 < BK / 2; ++k2) {
+        float a[2][8], b[2][8];
+        load2(as, bs, k2, a, b);
+        fma2k(a, b);
       }
-      if constexpr (!B_VK) {
+    } else {
+      float a[2][4][8], b[2][4][8];
+      load4(as, bs, 0, a[0], b[0]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float4 x = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 4 * tn);
-          const float4 y = *reinterpret_cast<const float4*>(bs + (4 * kk + k) * BL::LD + wn + 16 + 4 * tn);
-          b[k][0] = x.x; b[k][1] = x.y; b[k][2] = x.z; b[k][3] = x.w;
-          b[k][4] = y.x; b[k][5] = y.y; b[k][6] = y.z; b[k][7] = y.w;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float4 x = *reinterpret_cast<const float4*>(bs + (wn + tn + 4 * c) * BL::LD + 4 * kk);
-          b[0][c] = x.x; b[1][c] = x.y; b[2][c] = x.z; b[3][c] = x.w;
-        }
-      }
-      if constexpr (MODE == PAIR_C) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-          for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int c = 0; c < 8; c += 2)
-              ffma2(acc[r][c], acc[r][c + 1], a[k][r], a[k][r], b[k][c], b[k][c + 1]);
-      } else {   // PAIR_R
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-          for (int r = 0; r < 8; r += 2)
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              ffma2(acc[r][c], acc[r + 1][c], a[k][r], a[k][r + 1], b[k][c], b[k][c]);
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        if (kk + 1 < BK / 4) load4(as, bs, kk + 1, a[(kk + 1) & 1], b[(kk + 1) & 1]);
+        fma4(a[kk & 1], b[kk & 1]);
       }
     }
   }

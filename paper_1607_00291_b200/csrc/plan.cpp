@@ -256,21 +256,51 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
     p->scat[5] = scatter(p->b.J, 1);  // cscat_C
     if (p->k == 0) { p->scat[1].clear(); p->scat[2].clear(); }
   }
-  // Loader direction per operand: gather along the bundle whose first folded dim has unit
+  // GPU traversal order (DESIGN.md §3 R16; "the optimal ordering ... may differ
+  // from that achieved by the above heuristics"). The heuristic favours C's unit stride (sort
+  // by C stride) and A's only within P. On the GPU A and B are re-read N/128 and M/128 times
+  // while C is written once, so the kernel walks each bundle with an operand's unit-stride
+  // dimension first: A's (in I or else P), then B's (in P unless A took P's front, or J).
+  // Values are unchanged (same elements, other tile membership); the paper-order tables above
+  // stay the plan's reported scatter vectors.
+  p->kb = p->b;
+  auto unit_front = [](std::vector<Dim>& d, int w) {
+    for (size_t i = 0; i < d.size(); ++i)
+      if (d[i].s[w] == 1) {
+        if (i) { Dim x = d[i]; d.erase(d.begin() + (long)i); d.insert(d.begin(), x); }
+        return true;
+      }
+    return false;
+  };
+  bool a_m = unit_front(p->kb.I, 0);
+  bool a_k = !a_m && unit_front(p->kb.P, 0);
+  bool b_k = a_k ? (!p->kb.P.empty() && p->kb.P[0].s[1] == 1) : unit_front(p->kb.P, 1);
+  bool b_n = !b_k && unit_front(p->kb.J, 0);
+  (void)b_n;
+  if (!p->empty_out) {
+    p->kscat[0] = scatter(p->kb.I, 0);
+    p->kscat[1] = scatter(p->kb.P, 0);
+    p->kscat[2] = scatter(p->kb.P, 1);
+    p->kscat[3] = scatter(p->kb.J, 0);
+    p->kscat[4] = scatter(p->kb.I, 1);
+    p->kscat[5] = scatter(p->kb.J, 1);
+    if (p->k == 0) { p->kscat[1].clear(); p->kscat[2].clear(); }
+  }
+  // Loader direction per operand: gather along the bundle whose first dimension has unit
   // stride (16-byte vectors, coalesced warps); else along the smaller leading stride.
   auto lead = [](const std::vector<Dim>& d, int w) {
     return d.empty() ? INT64_MAX : std::llabs(d[0].s[w]);
   };
-  int64_t a_m = lead(p->b.I, 0), a_k = lead(p->b.P, 0);
-  int64_t b_k = lead(p->b.P, 1), b_n = lead(p->b.J, 0);
-  p->a_vec_m = a_m <= a_k;
-  p->b_vec_k = b_k <= b_n;
+  int64_t la_m = lead(p->kb.I, 0), la_k = lead(p->kb.P, 0);
+  int64_t lb_k = lead(p->kb.P, 1), lb_n = lead(p->kb.J, 0);
+  p->a_vec_m = la_m <= la_k;
+  p->b_vec_k = lb_k <= lb_n;
   if (!p->empty_out && p->k > 0) {
     const int64_t V = dtype == TC_F64 ? 2 : 4;
-    p->a_pairs_all = p->a_vec_m ? vec_blocks_all(p->scat[0], p->scat[1], V)
-                                : vec_blocks_all(p->scat[1], p->scat[0], V);
-    p->b_pairs_all = p->b_vec_k ? vec_blocks_all(p->scat[2], p->scat[3], V)
-                                : vec_blocks_all(p->scat[3], p->scat[2], V);
+    p->a_pairs_all = p->a_vec_m ? vec_blocks_all(p->kscat[0], p->kscat[1], V)
+                                : vec_blocks_all(p->kscat[1], p->kscat[0], V);
+    p->b_pairs_all = p->b_vec_k ? vec_blocks_all(p->kscat[2], p->kscat[3], V)
+                                : vec_blocks_all(p->kscat[3], p->kscat[2], V);
   }
   p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
                (dtype == TC_F32 ? 8 : 0);

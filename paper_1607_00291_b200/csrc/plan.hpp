@@ -61,6 +61,10 @@ struct Plan {
   bool empty_out = false;  // some free length is 0: no-op
   // scatter vectors, roles after the swap: 0 rA, 1 cA, 2 rB, 3 cB, 4 rC, 5 cC
   std::vector<int64_t> scat[6];
+  // GPU traversal order of the bundles (unit-stride dimensions of A, B first) and the scatter
+  // vectors the kernel walks (same elements, other linearisation)
+  Bundles kb;
+  std::vector<int64_t> kscat[6];
   bool a_vec_m = true;     // loader direction of A (true: along M)
   bool b_vec_k = true;     // loader direction of B (true: along K)
   bool idx64 = false;

@@ -137,13 +137,13 @@ static int get_tables(const Plan& p, DeviceTables** out) {
   d->device = dev;
   cudaDeviceGetAttribute(&d->num_sms, cudaDevAttrMultiProcessorCount, dev);
   for (int i = 0; i < 6; ++i) {
-    e = p.idx64 ? upload_table<long long>(p.scat[i], &d->tab[i])
-                : upload_table<int>(p.scat[i], &d->tab[i]);
+    e = p.idx64 ? upload_table<long long>(p.kscat[i], &d->tab[i])
+                : upload_table<int>(p.kscat[i], &d->tab[i]);
     if (e != cudaSuccess) { delete d; return cuda_fail(e, "table upload"); }
   }
   // A is gathered along rscat_A (M) or cscat_A (K); B along rscat_B (K) or cscat_B (N).
-  const std::vector<int64_t>& ta = p.a_vec_m ? p.scat[0] : p.scat[1];
-  const std::vector<int64_t>& tb = p.b_vec_k ? p.scat[2] : p.scat[3];
+  const std::vector<int64_t>& ta = p.a_vec_m ? p.kscat[0] : p.kscat[1];
+  const std::vector<int64_t>& tb = p.b_vec_k ? p.kscat[2] : p.kscat[3];
   const int64_t V = p.dtype == TC_F64 ? 2 : 4;
   std::vector<uint8_t> fa = vec_flags(ta, padded((int64_t)ta.size()), V);
   std::vector<uint8_t> fb = vec_flags(tb, padded((int64_t)tb.size()), V);
