@@ -122,6 +122,12 @@ int tc_plan_dim(const tc_plan* plan, int which, int idx, int64_t* len, int64_t* 
  * returns the length through *len. */
 int tc_plan_scatter(const tc_plan* plan, int which, int64_t* out, int64_t cap, int64_t* len);
 
+/* The scatter vectors the kernel actually walks (reading R16): the same six tables
+ * for the GPU traversal order of each bundle, which puts A's and then B's unit-stride dimension
+ * first. Same contraction, other linearisation; same arguments as tc_plan_scatter. */
+int tc_plan_traversal_scatter(const tc_plan* plan, int which, int64_t* out, int64_t cap,
+                              int64_t* len);
+
 /* Block-scatter vector of scatter vector `which` with block size b: entry i is the
  * common difference s > 0 of block i, else 0 (a one-entry block gives 1). */
 int tc_plan_block_scatter(const tc_plan* plan, int which, int64_t b, int64_t* out, int64_t cap,

@@ -32,6 +32,7 @@ ERRORS = {0: "TC_OK", 1: "TC_ERR_ARG", 2: "TC_ERR_LABEL", 3: "TC_ERR_SHAPE", 4: 
           5: "TC_ERR_UNSUPPORTED", 6: "TC_ERR_CUDA", 7: "TC_ERR_NOMEM"}
 EXPORTS = ["tc_contract", "tc_contract_host", "tc_plan_create", "tc_plan_execute",
            "tc_plan_destroy", "tc_plan_query", "tc_plan_dim", "tc_plan_scatter",
+           "tc_plan_traversal_scatter",
            "tc_plan_block_scatter", "tc_error_string", "tc_last_error_detail", "tc_version"]
 
 I64P = ctypes.POINTER(ctypes.c_int64)
@@ -63,6 +64,7 @@ _lib.tc_plan_query.argtypes = [ctypes.c_void_p, ctypes.POINTER(tc_plan_info)]
 _lib.tc_plan_dim.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, I64P, I64P, I64P,
                              ctypes.c_char_p, ctypes.c_int]
 _lib.tc_plan_scatter.argtypes = [ctypes.c_void_p, ctypes.c_int, I64P, ctypes.c_int64, I64P]
+_lib.tc_plan_traversal_scatter.argtypes = _lib.tc_plan_scatter.argtypes
 _lib.tc_plan_block_scatter.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, I64P,
                                        ctypes.c_int64, I64P]
 _lib.tc_error_string.argtypes = [ctypes.c_int]
@@ -232,6 +234,14 @@ class Plan:
         _check(_lib.tc_plan_scatter(self._p, which, None, 0, ctypes.byref(n)))
         arr = (ctypes.c_int64 * max(n.value, 1))()
         _check(_lib.tc_plan_scatter(self._p, which, arr, n.value, ctypes.byref(n)))
+        return list(arr)[: n.value]
+
+    def traversal_scatter(self, which: int):
+        """The tables the kernel walks (GPU traversal order, reading R16)."""
+        n = ctypes.c_int64()
+        _check(_lib.tc_plan_traversal_scatter(self._p, which, None, 0, ctypes.byref(n)))
+        arr = (ctypes.c_int64 * max(n.value, 1))()
+        _check(_lib.tc_plan_traversal_scatter(self._p, which, arr, n.value, ctypes.byref(n)))
         return list(arr)[: n.value]
 
     def block_scatter(self, which: int, b: int):

@@ -386,6 +386,17 @@ int tc_plan_scatter(const tc_plan* plan, int which, int64_t* out, int64_t cap, i
   return TC_OK;
 }
 
+int tc_plan_traversal_scatter(const tc_plan* plan, int which, int64_t* out, int64_t cap,
+                              int64_t* len) {
+  if (!plan || which < 0 || which > 5) return fail(TC_ERR_ARG, "bad argument");
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  const auto& v = p.kscat[which];
+  if (len) *len = (int64_t)v.size();
+  if (out)
+    for (int64_t i = 0; i < cap && i < (int64_t)v.size(); ++i) out[i] = v[(size_t)i];
+  return TC_OK;
+}
+
 int tc_plan_block_scatter(const tc_plan* plan, int which, int64_t b, int64_t* out, int64_t cap,
                           int64_t* len) {
   if (!plan || which < 0 || which > 5 || b <= 0) return fail(TC_ERR_ARG, "bad argument");

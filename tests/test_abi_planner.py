@@ -153,3 +153,32 @@ def test_planner_fig_bench_structures(idx):
 @pytest.mark.parametrize("i", range(7))
 def test_planner_rankk_structures(i):
     _compare(W.rankk(i, mn=60))
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_traversal_tables_reproduce_contraction(seed):
+    """The kernel's traversal-order tables (reading R16) are a relinearisation of the same
+    contraction: gathering through them and multiplying gives the brute-force result."""
+    import oracle
+    case = W.random_tiny_case(seed, max_len=5, dist="int")
+    A, B, C = W.make_tensors(case)
+    (la, sa, ta), (lb, sb, tb), (lc, sc, tcs) = _shapes(case)
+    p = tc.Plan(case.spec, case.dtype, (sa, sb, sc), (ta, tb, tcs))
+    flat = lambda T: torch.as_strided(T, (T.numel(),), (1,)).numpy()  # noqa: E731
+    a, b, c = flat(A), flat(B), flat(C)
+    if p.info()["swapped"]:
+        a, b = b, a
+    rA, cA, rB, cB, rC, cC = (np.array(p.traversal_scatter(i), dtype=np.int64) for i in range(6))
+    out = c.copy()
+    if len(cA):
+        new = case.alpha * (a[rA[:, None] + cA[None, :]] @ b[rB[:, None] + cB[None, :]])
+    else:
+        new = np.zeros((len(rC), len(cC)))
+    if case.beta != 0:
+        new = new + case.beta * c[rC[:, None] + cC[None, :]]
+    out[rC[:, None] + cC[None, :]] = new
+    ref = oracle.brute(case.spec, A.numpy(), B.numpy(), C.numpy(), case.alpha, case.beta)
+    assert np.array_equal(out, np.asarray(ref).reshape(-1, order="F"))
+    # and it is the paper-order table set up to a permutation of rows/columns
+    for i in range(6):
+        assert sorted(p.traversal_scatter(i)) == sorted(p.scatter(i))
