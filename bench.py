@@ -37,6 +37,27 @@ import workloads as W  # noqa: E402
 
 SHARD_LABELS = "abc"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "PEAKS_FP64.json")
+# DRAM bytes per launch of the contraction kernel on the full cfg5 workload, from
+# `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum` of this same
+# command (tools/gpu/r01_checkpoint.sh); the counters of the `--set full` memory section.
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01", "traffic_cfg5_full.csv")
+
+
+def ncu_traffic(path, kernel_prefix="tc_dmma_ws_kernel"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the first profiled launch of the kernel."""
+    import csv
+    if not os.path.exists(path):
+        return None
+    vals = {}
+    for r in csv.reader(open(path)):
+        if len(r) < 15 or r[0] == "ID" or kernel_prefix not in r[4]:
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(r[13])
+        if scale and r[12] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            vals.setdefault(r[12], float(r[14].replace(",", "")) * scale)
+    if len(vals) != 2:
+        return None
+    return int(sum(vals.values()))
 SMI_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -382,11 +403,13 @@ def run_native(args):
             "contraction_over_gemm": round(achieved_tf / gemm_tf, 4)},
         "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 3),
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
-                     "traffic": None,
+                     "traffic": None if args.small or world > 1 else ncu_traffic(TRAFFIC_FILE),
+                     "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, one "
+                                       "launch of this workload (profiles/r01/traffic_cfg5_full.csv)",
                      "peak_source": "profiles/PEAKS_FP64.json dmma_tflops (measured DMMA.8x8x4 "
                                     "loop on this pool's B200; fp64 has no entry in "
                                     "MEASURED_PEAKS.json)",
-                     "kernel": "tc_dmma_f64_kernel", "kernel_ms": round(kernel_ms, 3),
+                     "kernel": "tc_dmma_ws_kernel (persistent, warp-specialised DMMA)", "kernel_ms": round(kernel_ms, 3),
                      "algorithmic_flops_per_launch": flops_rank},
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": args.steps * world,
         "finite_output": finite,
