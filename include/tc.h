@@ -76,13 +76,21 @@ typedef struct tc_plan tc_plan;
 int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                 double beta, const tc_tensor* C, void* stream);
 
-/* Same operation on HOST buffers (end-to-end path): copies the address span of A, B (and of C
- * when beta != 0) to device memory the call allocates on `stream`, runs tc_contract, copies
- * C's span back, frees, and synchronises `stream` before returning. Pinned host memory gives
- * full copy bandwidth; pageable memory works. Elements of C's span that are not elements of C
- * are preserved. */
+/* Same operation on HOST buffers (the end-to-end path). Copies the address spans of A and B
+ * (and of C when beta != 0, or when C's span has holes) to device staging memory, contracts,
+ * copies C's span back, and synchronises `stream` before returning. The work is cut into up
+ * to 8 chunks along one free label of C (the one with C's largest stride whose chunks are
+ * disjoint address intervals and which adds at most 5% copy volume), so host->device copies,
+ * kernels and device->host copies of consecutive chunks overlap on three streams; otherwise a
+ * single chunk. Pinned host memory gives full copy bandwidth and overlap; pageable memory
+ * works. Elements of C's span that are not elements of C are preserved. The staging memory
+ * (the spans of A, B, C) is kept per device between calls; tc_release_staging() frees it.
+ * Calls on one device are serialised by an internal lock. */
 int tc_contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                      double beta, const tc_tensor* C, void* stream);
+
+/* Free the device staging memory tc_contract_host keeps (all devices). Returns TC_OK. */
+int tc_release_staging(void);
 
 /* Plan from shapes/strides/labels only (the `data` fields are ignored). Host-only: needs no GPU.
  * On success *plan owns its tables; release with tc_plan_destroy. */

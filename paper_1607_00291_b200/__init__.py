@@ -30,7 +30,7 @@ TC_F64, TC_F32 = 0, 1
 TC_MAX_RANK = 16
 ERRORS = {0: "TC_OK", 1: "TC_ERR_ARG", 2: "TC_ERR_LABEL", 3: "TC_ERR_SHAPE", 4: "TC_ERR_ALIAS",
           5: "TC_ERR_UNSUPPORTED", 6: "TC_ERR_CUDA", 7: "TC_ERR_NOMEM"}
-EXPORTS = ["tc_contract", "tc_contract_host", "tc_plan_create", "tc_plan_execute",
+EXPORTS = ["tc_contract", "tc_contract_host", "tc_release_staging", "tc_plan_create", "tc_plan_execute",
            "tc_plan_destroy", "tc_plan_query", "tc_plan_dim", "tc_plan_scatter",
            "tc_plan_traversal_scatter",
            "tc_plan_block_scatter", "tc_error_string", "tc_last_error_detail", "tc_version"]
@@ -253,6 +253,11 @@ class Plan:
 
 
 SCATTER_NAMES = ["rscat_A", "cscat_A", "rscat_B", "cscat_B", "rscat_C", "cscat_C"]
+
+
+def release_staging() -> None:
+    """Free the device staging memory contract_host keeps between calls (tc_release_staging)."""
+    _check(_lib.tc_release_staging())
 
 
 def version() -> int:

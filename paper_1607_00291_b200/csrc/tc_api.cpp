@@ -254,6 +254,213 @@ static bool overlaps(const tc_tensor* X, const tc_tensor* C, size_t esz) {
   return x0 < c1 && c0 < x1;
 }
 
+// ---- end-to-end path on host buffers (tc_contract_host) ------------------------------------
+// The work is cut into chunks along one free label x of C (a contiguous range of x per chunk,
+// a free sub-block of C is an independent contraction whose operands are strided
+// sub-views). Host->device copies of chunk i+1, the contraction of chunk i and the
+// device->host copy of chunk i-1 run on three streams at once, so the PCIe transfers hide
+// behind the kernel. x is chosen so that C's chunks are disjoint address intervals (x has the
+// largest stride of C) and the bytes copied are minimal; when no label qualifies, one chunk.
+// Device staging buffers are kept per device between calls (tc_release_staging frees them).
+struct Staging {
+  void* buf[3] = {nullptr, nullptr, nullptr};
+  size_t cap[3] = {0, 0, 0};
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+static std::mutex g_stage_mu;
+static std::map<int, Staging> g_stage;
+
+static cudaError_t stage_reserve(Staging& st, int t, size_t bytes) {
+  if (st.cap[t] >= bytes) return cudaSuccess;
+  if (st.buf[t]) { cudaFree(st.buf[t]); st.buf[t] = nullptr; st.cap[t] = 0; }
+  cudaError_t e = cudaMalloc(&st.buf[t], bytes);
+  if (e == cudaSuccess) st.cap[t] = bytes;
+  return e;
+}
+
+static int label_pos(const tc_tensor* T, char x) {
+  for (int d = 0; d < T->rank; ++d)
+    if (T->labels[d] == x) return d;
+  return -1;
+}
+
+// Chunks along dimension `pos` are disjoint address intervals: a positive stride larger than
+// the span of all other dimensions.
+static bool outer_dim(const tc_tensor* T, int pos) {
+  const int64_t s = T->strides[pos];
+  if (s <= 0) return false;
+  int64_t ext = 0;
+  for (int d = 0; d < T->rank; ++d)
+    if (d != pos) ext += (T->strides[d] < 0 ? -T->strides[d] : T->strides[d]) * (T->lens[d] - 1);
+  return s > ext;
+}
+
+struct Piece {           // the address span [lo, hi] (elements, relative to data) of a sub-view
+  int64_t lo = 1, hi = 0;
+  int64_t bytes(size_t esz) const { return lo <= hi ? (hi - lo + 1) * (int64_t)esz : 0; }
+};
+
+// Span of T restricted to x in [x0, x0 + len) along dimension pos (pos < 0: whole tensor).
+static Piece piece_of(const tc_tensor* T, int pos, int64_t x0, int64_t len) {
+  Piece p;
+  int64_t lens[TC_MAX_RANK];
+  for (int d = 0; d < T->rank; ++d) lens[d] = T->lens[d];
+  int64_t off = 0;
+  if (pos >= 0) { lens[pos] = len; off = x0 * T->strides[pos]; }
+  span(T->rank, lens, T->strides, &p.lo, &p.hi);
+  if (p.lo <= p.hi) { p.lo += off; p.hi += off; }
+  return p;
+}
+
+constexpr int kHostChunks = 8;
+constexpr int64_t kHostChunkMinBytes = 64ll << 20;
+
+static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
+                         double beta, const tc_tensor* C, cudaStream_t s) {
+  std::shared_ptr<Plan> full;
+  int rc = get_plan(dtype, A, B, C, &full);
+  if (rc != TC_OK) return rc;
+  const size_t esz = dtype == TC_F64 ? 8 : 4;
+  if (overlaps(A, C, esz) || overlaps(B, C, esz)) return fail(TC_ERR_ALIAS, "C overlaps A or B");
+  if (full->empty_out) return TC_OK;
+  const bool need_ab = alpha != 0.0 && full->k > 0;
+  const tc_tensor* T[3] = {A, B, C};
+  for (int t = 0; t < 3; ++t)
+    if ((t == 2 || need_ab) && !T[t]->data) return fail(TC_ERR_ARG, "null host data pointer");
+  int64_t nC = 1;
+  for (int d = 0; d < C->rank; ++d) nC *= C->lens[d];
+  Piece whole[3];
+  for (int t = 0; t < 3; ++t) whole[t] = piece_of(T[t], -1, 0, 0);
+  // C is uploaded when it is read (beta != 0) or when its span has holes that must survive
+  auto c_upload = [&](const Piece& pc, int64_t elems) {
+    return beta != 0.0 || (pc.lo <= pc.hi && pc.hi - pc.lo + 1 != elems);
+  };
+  const int64_t unsplit = (need_ab ? whole[0].bytes(esz) + whole[1].bytes(esz) : 0) +
+                          whole[2].bytes(esz) * (c_upload(whole[2], nC) ? 2 : 1);
+
+  // -- choose the chunk label x (in C and in exactly one operand X; Y is the other operand)
+  int best_c = -1, best_x = -1, best_t = -1;
+  int64_t best_q = 0, best_cost = 0, best_len = 0;
+  if (need_ab && unsplit >= kHostChunkMinBytes) {
+    for (int pc = 0; pc < C->rank; ++pc) {
+      const int64_t len = C->lens[pc];
+      if (len < 2 || !outer_dim(C, pc)) continue;
+      const int xt = label_pos(A, C->labels[pc]) >= 0 ? 0 : 1;
+      const int px = label_pos(T[xt], C->labels[pc]);
+      if (px < 0) continue;
+      const int64_t q = (len + kHostChunks - 1) / kHostChunks;
+      int64_t cost = whole[1 - xt].bytes(esz);
+      for (int64_t x0 = 0; x0 < len; x0 += q) {
+        const int64_t l = std::min(q, len - x0);
+        const Piece pcx = piece_of(C, pc, x0, l);
+        cost += piece_of(T[xt], px, x0, l).bytes(esz) +
+                pcx.bytes(esz) * (c_upload(pcx, nC / len * l) ? 2 : 1);
+      }
+      if (cost * 20 > unsplit * 21) continue;  // more than 5% extra copy volume
+      if (best_c < 0 || cost < best_cost || (cost == best_cost && len > best_len)) {
+        best_c = pc; best_x = px; best_t = xt; best_q = q; best_cost = cost; best_len = len;
+      }
+    }
+  }
+  const int nch = best_c < 0 ? 1 : (int)((best_len + best_q - 1) / best_q);
+
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  Staging& st = g_stage[dev];
+  if (!st.h2d) {
+    if ((e = cudaStreamCreateWithFlags(&st.h2d, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&st.d2h, cudaStreamNonBlocking)) != cudaSuccess)
+      return cuda_fail(e, "stream creation");
+  }
+  const char* dbase[3] = {nullptr, nullptr, nullptr};
+  for (int t = 0; t < 3; ++t) {
+    if ((t < 2 && !need_ab) || whole[t].lo > whole[t].hi) continue;
+    if ((e = stage_reserve(st, t, (size_t)whole[t].bytes(esz))) != cudaSuccess)
+      return cuda_fail(e, "staging allocation");
+    dbase[t] = static_cast<const char*>(st.buf[t]) - whole[t].lo * (int64_t)esz;
+  }
+  auto h2d = [&](int t, const Piece& p) {
+    if (p.lo > p.hi) return cudaSuccess;
+    return cudaMemcpyAsync(const_cast<char*>(dbase[t]) + p.lo * (int64_t)esz,
+                           static_cast<const char*>(T[t]->data) + p.lo * (int64_t)esz,
+                           (size_t)p.bytes(esz), cudaMemcpyHostToDevice, st.h2d);
+  };
+
+  std::vector<cudaEvent_t> ev;
+  auto event = [&](cudaEvent_t* out) {
+    cudaError_t r = cudaEventCreateWithFlags(out, cudaEventDisableTiming);
+    if (r == cudaSuccess) ev.push_back(*out);
+    return r;
+  };
+  cudaEvent_t e_start = nullptr, e_y = nullptr, e_end = nullptr;
+  std::vector<cudaEvent_t> e_in((size_t)nch, nullptr), e_out((size_t)nch, nullptr);
+  if ((e = event(&e_start)) == cudaSuccess && (e = event(&e_y)) == cudaSuccess)
+    e = event(&e_end);
+  for (int i = 0; i < nch && e == cudaSuccess; ++i)
+    if ((e = event(&e_in[(size_t)i])) == cudaSuccess) e = event(&e_out[(size_t)i]);
+  // work already queued on `stream` (e.g. the producer of the host inputs) comes first
+  if (e == cudaSuccess) e = cudaEventRecord(e_start, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st.h2d, e_start, 0);
+  // Y (the operand without x) in full, then X and C chunk by chunk
+  const int yt = best_c < 0 ? -1 : 1 - best_t;
+  if (e == cudaSuccess && yt >= 0) e = h2d(yt, whole[yt]);
+  if (e == cudaSuccess) e = cudaEventRecord(e_y, st.h2d);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, e_y, 0);
+  for (int i = 0; i < nch && e == cudaSuccess && rc == TC_OK; ++i) {
+    const int64_t x0 = i * best_q, l = best_c < 0 ? 0 : std::min(best_q, best_len - x0);
+    // the chunk as tensors: x restricted to [x0, x0 + l)
+    int64_t lens[3][TC_MAX_RANK];
+    tc_tensor sub[3];
+    Piece pp[3];
+    int64_t off[3] = {0, 0, 0};
+    for (int t = 0; t < 3; ++t) {
+      sub[t] = *T[t];
+      for (int d = 0; d < T[t]->rank; ++d) lens[t][d] = T[t]->lens[d];
+      sub[t].lens = lens[t];
+      const int pos = best_c < 0 ? -1 : (t == 2 ? best_c : (t == best_t ? best_x : -1));
+      if (pos >= 0) { lens[t][pos] = l; off[t] = x0 * T[t]->strides[pos]; }
+      pp[t] = piece_of(T[t], pos, x0, l);
+    }
+    if (best_c < 0) {
+      if (need_ab) {
+        if ((e = h2d(0, pp[0])) != cudaSuccess || (e = h2d(1, pp[1])) != cudaSuccess) break;
+      }
+    } else if ((e = h2d(best_t, pp[best_t])) != cudaSuccess) {
+      break;
+    }
+    int64_t nCi = 1;
+    for (int d = 0; d < C->rank; ++d) nCi *= lens[2][d];
+    if (c_upload(pp[2], nCi) && (e = h2d(2, pp[2])) != cudaSuccess) break;
+    if ((e = cudaEventRecord(e_in[(size_t)i], st.h2d)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(s, e_in[(size_t)i], 0)) != cudaSuccess) break;
+    std::shared_ptr<Plan> p = full;
+    if (best_c >= 0 && (rc = get_plan(dtype, &sub[0], &sub[1], &sub[2], &p)) != TC_OK) break;
+    const char* dp[3];
+    for (int t = 0; t < 3; ++t) dp[t] = dbase[t] ? dbase[t] + off[t] * (int64_t)esz : nullptr;
+    if ((rc = execute(*p, alpha, dp[0], dp[1], beta, const_cast<char*>(dp[2]), s)) != TC_OK) break;
+    if ((e = cudaEventRecord(e_out[(size_t)i], s)) != cudaSuccess) break;
+    if ((e = cudaStreamWaitEvent(st.d2h, e_out[(size_t)i], 0)) != cudaSuccess) break;
+    if (pp[2].lo <= pp[2].hi)
+      e = cudaMemcpyAsync(static_cast<char*>(C->data) + pp[2].lo * (int64_t)esz,
+                          dbase[2] + pp[2].lo * (int64_t)esz, (size_t)pp[2].bytes(esz),
+                          cudaMemcpyDeviceToHost, st.d2h);
+  }
+  // `stream` completes after the last copy back, whatever happened above
+  cudaError_t e2 = cudaEventRecord(e_end, st.d2h);
+  if (e2 == cudaSuccess) e2 = cudaStreamWaitEvent(s, e_end, 0);
+  cudaError_t e3 = cudaStreamSynchronize(st.h2d);
+  cudaError_t e4 = cudaStreamSynchronize(st.d2h);
+  cudaError_t e5 = cudaStreamSynchronize(s);
+  for (auto x : ev) cudaEventDestroy(x);
+  if (e != cudaSuccess) return cuda_fail(e, "host path copy");
+  if (rc != TC_OK) return rc;
+  for (cudaError_t x : {e2, e3, e4, e5})
+    if (x != cudaSuccess) return cuda_fail(x, "host path synchronize");
+  return TC_OK;
+}
+
 }  // namespace tcb
 
 using namespace tcb;
@@ -273,50 +480,19 @@ int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tenso
 
 int tc_contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                      double beta, const tc_tensor* C, void* stream) {
-  std::shared_ptr<Plan> p;
-  int rc = get_plan(dtype, A, B, C, &p);
-  if (rc != TC_OK) return rc;
-  size_t esz = dtype == TC_F64 ? 8 : 4;
-  if (overlaps(A, C, esz) || overlaps(B, C, esz))
-    return fail(TC_ERR_ALIAS, "C overlaps A or B");
-  if (p->empty_out) return TC_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const tc_tensor* T[3] = {A, B, C};
-  void* dbuf[3] = {nullptr, nullptr, nullptr};
-  const char* dbase[3] = {nullptr, nullptr, nullptr};
-  int64_t lo[3], hi[3];
-  bool need_ab = alpha != 0.0 && p->k > 0;
-  cudaError_t e = cudaSuccess;
-  int64_t n_elems_c = 1;
-  for (int i = 0; i < C->rank; ++i) n_elems_c *= C->lens[i];
-  for (int t = 0; t < 3 && e == cudaSuccess; ++t) {
-    span(T[t]->rank, T[t]->lens, T[t]->strides, &lo[t], &hi[t]);
-    if (t < 2 && !need_ab) continue;
-    if (lo[t] > hi[t]) continue;
-    size_t bytes = (size_t)(hi[t] - lo[t] + 1) * esz;
-    if (!T[t]->data) { e = cudaErrorInvalidValue; break; }
-    e = cudaMallocAsync(&dbuf[t], bytes, s);
-    if (e != cudaSuccess) break;
-    dbase[t] = static_cast<const char*>(dbuf[t]) - lo[t] * (int64_t)esz;
-    const char* src = static_cast<const char*>(T[t]->data) + lo[t] * (int64_t)esz;
-    // C's span is uploaded when C is read (beta != 0) or has holes that must survive
-    bool upload = t < 2 || beta != 0.0 || (hi[t] - lo[t] + 1) != n_elems_c;
-    if (upload) e = cudaMemcpyAsync(dbuf[t], src, bytes, cudaMemcpyHostToDevice, s);
+  return contract_host(dtype, alpha, A, B, beta, C, static_cast<cudaStream_t>(stream));
+}
+
+int tc_release_staging(void) {
+  std::lock_guard<std::mutex> lk(g_stage_mu);
+  int cur = -1;
+  cudaGetDevice(&cur);
+  for (auto& kv : g_stage) {
+    cudaSetDevice(kv.first);
+    for (auto& b : kv.second.buf) { cudaFree(b); b = nullptr; }
+    for (auto& c : kv.second.cap) c = 0;
   }
-  if (e == cudaSuccess) {
-    rc = execute(*p, alpha, dbase[0], dbase[1], beta, const_cast<char*>(dbase[2]), s);
-    if (rc == TC_OK && lo[2] <= hi[2]) {
-      size_t bytes = (size_t)(hi[2] - lo[2] + 1) * esz;
-      e = cudaMemcpyAsync(static_cast<char*>(C->data) + lo[2] * (int64_t)esz, dbuf[2], bytes,
-                          cudaMemcpyDeviceToHost, s);
-    }
-  }
-  for (auto* b : dbuf)
-    if (b) cudaFreeAsync(b, s);
-  cudaError_t e2 = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return cuda_fail(e, "host path copy");
-  if (rc != TC_OK) return rc;
-  if (e2 != cudaSuccess) return cuda_fail(e2, "host path synchronize");
+  if (cur >= 0) cudaSetDevice(cur);
   return TC_OK;
 }
 

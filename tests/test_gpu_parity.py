@@ -295,6 +295,71 @@ def test_host_path_end_to_end():
     assert relerr(Cp.numpy(), ref.numpy()) < 1e-12
 
 
+def _host_vs_device(case, C_host_big=None):
+    """contract_host on pinned host tensors vs contract on the device, integer inputs (pin p5:
+    every partial sum exact, so both must be bitwise equal whatever the chunking)."""
+    A, B, C = W.make_tensors(case, "cpu")
+    Ap, Bp = A.pin_memory(), B.pin_memory()
+    Cp = W.colmajor_view(torch.empty(C.numel(), dtype=C.dtype).pin_memory(), list(C.shape))
+    Cp.copy_(C)
+    Ad, Bd, Cd = A.cuda(), B.cuda(), C.cuda()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    tc().contract_host(case.spec, Ap, Bp, Cp, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    assert torch.equal(Cp, Cd.cpu()), case.name
+    return A, B, C, Cp
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_host_path_chunked_cfg5_structure(beta):
+    """cfg5's structure at 24/12 (A 191 MB): the host path cuts C into chunks along k (C's and
+    B's outermost label) and pipelines copies with kernels; equal to the device path bitwise
+    (integer mode) and to the oracle on a sampled sub-block."""
+    case = W.cfg5(24, 12)
+    case.dist, case.alpha, case.beta, case.c_init = "int", 1.0, beta, "dist"
+    A, B, C, Cp = _host_vs_device(case)
+    e, c1, _ = sampled_check(case, A, B, C, Cp, per_label=2)
+    assert e == 0.0
+
+
+def test_host_path_chunked_beta_and_scattered_C():
+    """cfg3 variant (C stored aibj, beta = 1 so C chunks are uploaded too), 134 MB operands."""
+    case = W.cfg3(True, v=64, o=32)
+    case.dist, case.alpha, case.beta = "int", 0.5, 1.0
+    A, B, C, Cp = _host_vs_device(case)
+    e, _, _ = sampled_check(case, A, B, C, Cp, per_label=3)
+    assert e == 0.0
+
+
+def test_host_path_chunked_C_with_holes():
+    """C is a sub-view of a larger pinned buffer: chunks along n (C's outer stride) copy spans
+    that include the holes, which must come back unchanged."""
+    g = torch.Generator().manual_seed(11)
+    m, n, k = 4090, 1000, 2048
+    A = torch.randint(-4, 5, (k, m), generator=g).double().t()          # (m, k) strides (1, m)
+    B = torch.randint(-4, 5, (n, k), generator=g).double().t()          # (k, n) strides (1, k)
+    big = torch.randint(-4, 5, (1003, 4096), generator=g).double().pin_memory()
+    Cv = big.t()[:m, 1:n + 1]                                            # strides (1, 4096)
+    keep = big.clone()
+    ref_dev = Cv.cuda()
+    tc().contract("mn-mk-kn", A.cuda(), B.cuda(), ref_dev, 2.0, 0.0)
+    tc().contract_host("mn-mk-kn", A.pin_memory(), B.pin_memory(), Cv, 2.0, 0.0)
+    assert torch.equal(Cv, ref_dev.cpu())
+    mask = torch.ones_like(big, dtype=torch.bool)
+    mask.t()[:m, 1:n + 1] = False
+    assert torch.equal(big[mask], keep[mask])
+
+
+def test_host_path_release_staging():
+    case = W.cfg3(False, v=16, o=8)
+    A, B, C = W.make_tensors(case, "cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    tc().contract_host(case.spec, A, B, C, case.alpha, case.beta)   # pageable memory
+    tc().release_staging()
+    assert relerr(C.numpy(), ref.numpy()) < 1e-12
+
+
 def test_repeat_calls_bitwise_deterministic():
     case = W.cfg4(5)
     Ad, Bd, Cd = W.make_tensors(case, "cuda")
