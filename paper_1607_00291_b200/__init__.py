@@ -18,7 +18,7 @@ import os
 from typing import Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtc_b200.so")
+LIB_PATH = os.environ.get("TC_B200_LIB") or os.path.join(_HERE, "libtc_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python __graft_entry__.py build` "

@@ -12,10 +12,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libtc_b200.so")
-OBJ = os.path.join(HERE, "build_obj")
-SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "ws_f64.cu", "ws_f32_ffma.cu",
-           "ws_f32_dmma.cu"]
+# TC_LIB_OUT / TC_NVCC_EXTRA: build a variant library elsewhere with extra nvcc flags (kernel
+# A/B experiments, e.g. -DTC_STAGES_F32=4); load it with TC_B200_LIB=<path>.
+LIB = os.environ.get("TC_LIB_OUT") or os.path.join(HERE, "libtc_b200.so")
+OBJ = os.path.join(HERE, "build_obj") if not os.environ.get("TC_LIB_OUT") else LIB + ".obj"
+EXTRA = os.environ.get("TC_NVCC_EXTRA", "").split()
+SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu",
+           "ws_f64_a0.cu", "ws_f64_a1.cu", "ws_f64_a2.cu",
+           "ws_f32_ffma_a0.cu", "ws_f32_ffma_a1.cu", "ws_f32_ffma_a2.cu", "ws_f32_dmma.cu"]
 HEADERS = ["plan.hpp", "kernels.hpp", "dev_common.cuh", "contract_ws.cuh"]
 
 NVCC_FLAGS = [
@@ -36,7 +40,7 @@ def _stale() -> bool:
 
 def _compile(nvcc: str, src: str):
     obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
+    cmd = [nvcc, *NVCC_FLAGS, *EXTRA, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
            os.path.join(CSRC, src), "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, cmd, res
@@ -65,7 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         failed = res.returncode != 0
         if failed:
             sys.stderr.write(res.stderr[-6000:])
-    with open(os.path.join(HERE, "build.log"), "w") as f:
+    with open(os.path.join(HERE, "build.log") if LIB.startswith(HERE) else LIB + ".log", "w") as f:
         f.write("\n".join(log))
     if failed:
         raise RuntimeError("nvcc build of libtc_b200.so failed (see paper_1607_00291_b200/build.log)")

@@ -322,13 +322,37 @@ int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-int launch_ws_f64(const LaunchArgs& a, cudaStream_t stream);        // ws_f64.cu
-int launch_ws_f32_ffma(const LaunchArgs& a, cudaStream_t stream);   // ws_f32_ffma.cu
+// ws_<type>_a<mode>.cu: one translation unit per (element type, A gather mode)
+int launch_ws_f64_a0(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f64_a1(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f64_a2(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f64_idx64(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f32_ffma_a0(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f32_ffma_a1(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f32_ffma_a2(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f32_ffma_idx64(const LaunchArgs& a, cudaStream_t stream);
 int launch_ws_f32_dmma(const LaunchArgs& a, cudaStream_t stream);   // ws_f32_dmma.cu
 
-static int launch_ws(const LaunchArgs& a, cudaStream_t stream) {
-  if (!a.f32) return launch_ws_f64(a, stream);
-  return a.f32_dmma ? launch_ws_f32_dmma(a, stream) : launch_ws_f32_ffma(a, stream);
+// Gather mode per operand: vectors when the plan proved every vector contiguous and aligned,
+// else the coalesced element gather or the per-vector check, as the plan prefers.
+static int launch_ws(const LaunchArgs& args, cudaStream_t stream) {
+  LaunchArgs a = args;
+  a.a_mode = a.a_vec_all ? 0 : (a.a_elem ? 2 : 1);
+  a.b_mode = a.b_vec_all ? 0 : (a.b_elem ? 2 : 1);
+  if (a.f32 && a.f32_dmma) return launch_ws_f32_dmma(a, stream);
+  if (a.idx64) return a.f32 ? launch_ws_f32_ffma_idx64(a, stream) : launch_ws_f64_idx64(a, stream);
+  if (a.f32) {
+    switch (a.a_mode) {
+      case 0: return launch_ws_f32_ffma_a0(a, stream);
+      case 1: return launch_ws_f32_ffma_a1(a, stream);
+      default: return launch_ws_f32_ffma_a2(a, stream);
+    }
+  }
+  switch (a.a_mode) {
+    case 0: return launch_ws_f64_a0(a, stream);
+    case 1: return launch_ws_f64_a1(a, stream);
+    default: return launch_ws_f64_a2(a, stream);
+  }
 }
 
 // Kernel selection: the warp-specialised kernel (contract_ws.cu, fp64 and fp32) is the default;

@@ -36,7 +36,19 @@ constexpr int NPW = 4;                      // producer warps
 constexpr int NPT = NPW * 32;               // producer threads
 constexpr int NTHREADS = (NCW + NPW) * 32;
 constexpr int WM = 64, WN = 32;
-constexpr int STAGES = 4;
+constexpr int kWarpTab = WM + WN;           // C scatter entries per consumer warp and tile
+// Ring depth per element type: an fp32 K step computes in half the time of an fp64 one (FFMA
+// at 2x the DMMA rate) and moves half the bytes, so it needs twice the stages in flight to
+// cover the same copy latency.
+#ifndef TC_STAGES_F32
+#define TC_STAGES_F32 8
+#endif
+#ifndef TC_STAGES_F64
+#define TC_STAGES_F64 4
+#endif
+template <typename T> constexpr int stages() {
+  return sizeof(T) == 4 ? TC_STAGES_F32 : TC_STAGES_F64;
+}
 constexpr int GROUP_M = 8;
 // setmaxnreg budgets: 128 x 56 + 256 x 224 = 64512 <= 65536 registers per SM, and per SMSP
 // (warps w, w+4, w+8) 224 + 224 + 56 = 504 <= 512 registers per lane.
@@ -105,6 +117,10 @@ struct Gather {
   uint32_t vm;                             // FIXED_VECS: bit e = entry e valid, bit V = contiguous
   IDX ro[NS];                              // K_VECS: offsets of the thread's tile rows
   uint32_t rv;                             // K_VECS: bit i = row i in range
+  // K-table entries of the next stage, loaded one stage ahead (load_k) so that their latency
+  // overlaps the wait for a free ring slot instead of delaying the copies
+  IDX kv[FIXED_VECS ? NS : V];
+  bool kvec;                               // K_VECS: the thread's V K-entries are contiguous
 
   __device__ __forceinline__ void init(const IDX* __restrict__ tab,
                                        const uint8_t* __restrict__ flags, int base,
@@ -130,15 +146,30 @@ struct Gather {
     }
   }
 
-  __device__ __forceinline__ void issue(T* sm, const T* __restrict__ g,
-                                        const IDX* __restrict__ ktab,
-                                        const uint8_t* __restrict__ kflags, int k0, int K,
-                                        int p) {
+  // K-table entries this thread needs for the stage starting at k0 (tables are padded by at
+  // least 128 entries, so reads past K are in bounds; their copies are predicated off).
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab,
+                                         const uint8_t* __restrict__ kflags, int k0, int K,
+                                         int p) {
     if constexpr (FIXED_VECS) {
       const int rg = p / (128 / V);
-      IDX kv[NS];
 #pragma unroll
       for (int i = 0; i < NS; ++i) kv[i] = __ldg(ktab + k0 + rg + V * i);
+    } else {
+      const int k = k0 + V * (p % (16 / V));
+      if constexpr (VEC) {
+        kv[0] = __ldg(ktab + k);
+      } else {
+#pragma unroll
+        for (int j = 0; j < V; ++j) kv[j] = __ldg(ktab + k + j);
+        kvec = (k + V - 1 < K) && __ldg(kflags + k / V);
+      }
+    }
+  }
+
+  __device__ __forceinline__ void issue(T* sm, const T* __restrict__ g, int k0, int K, int p) {
+    if constexpr (FIXED_VECS) {
+      const int rg = p / (128 / V);
       T* d0 = sm + V * (p % (128 / V));
 #pragma unroll
       for (int i = 0; i < NS; ++i) {
@@ -163,35 +194,100 @@ struct Gather {
       const int k = k0 + V * kq;
       T* d0 = sm + V * kq;
       if constexpr (VEC) {
-        const IDX c0 = __ldg(ktab + k);
         const bool kin = k < K;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
           const int r = p / (16 / V) + 8 * V * i;
-          cp_async16(d0 + r * LD, g + (ro[i] + c0), kin && ((rv >> i) & 1u));
+          cp_async16(d0 + r * LD, g + (ro[i] + kv[0]), kin && ((rv >> i) & 1u));
         }
       } else {
-        IDX c[V];
-#pragma unroll
-        for (int j = 0; j < V; ++j) c[j] = __ldg(ktab + k + j);
-        const bool kvec = (k + V - 1 < K) && __ldg(kflags + k / V);
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
           const int r = p / (16 / V) + 8 * V * i;
           const bool rin = (rv >> i) & 1u;
           T* d = d0 + r * LD;
-          const T* p0 = g + (ro[i] + c[0]);
+          const T* p0 = g + (ro[i] + kv[0]);
           if (kvec && rin) {
             copy_contig(d, p0);
           } else {
 #pragma unroll
             for (int j = 0; j < V; ++j)
-              cp_async_elem(d + j, g + (ro[i] + c[j]), rin && (k + j < K));
+              cp_async_elem(d + j, g + (ro[i] + kv[j]), rin && (k + j < K));
           }
         }
       }
     }
   }
+};
+
+// Coalesced element gather (mode 2), for operands whose 16-byte vectors are often not
+// contiguous or not aligned (short or odd unit-stride runs): every copy moves one element, and
+// the 32 lanes of a warp take 32 consecutive entries of the gather direction, so when the
+// entries are consecutive addresses one warp instruction reads one 128-byte (fp32) or 256-byte
+// (fp64) run instead of 32 lane-strided pieces.
+//  FIXED_VECS (gathered along the tile's own bundle, [k][row] layout): lane l owns bundle
+//              entries l + 32 j (j < 4), fixed for the tile; warp w owns K rows 4 w + i.
+//  K_VECS     ([row][k] layout): lane l owns K entry l % 16 of every stage and tile rows
+//              32 w + 2 q + l / 16 (q < 16), whose offsets it keeps.
+// Each thread issues 16 element copies per stage either way.
+template <typename T, typename IDX, bool FIXED_VECS, int LD>
+struct GatherElem {
+  static constexpr int NR = FIXED_VECS ? 4 : 16;   // fixed offsets per thread
+  IDX o[NR];
+  uint32_t valid;                                  // bit q: fixed entry q in range
+  IDX kv[FIXED_VECS ? 4 : 1];                      // next stage's K entries (load_k)
+
+  __device__ __forceinline__ void init(const IDX* __restrict__ tab, const uint8_t*, int base,
+                                       int extent, int p) {
+    const int w = p >> 5, l = p & 31;
+    valid = 0;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int e = FIXED_VECS ? base + l + 32 * q : base + 32 * w + 2 * q + (l >> 4);
+      o[q] = tab[e];
+      valid |= (e < extent ? 1u : 0u) << q;
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, const uint8_t*, int k0,
+                                         int, int p) {
+    if constexpr (FIXED_VECS) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) kv[i] = __ldg(ktab + k0 + 4 * (p >> 5) + i);
+    } else {
+      kv[0] = __ldg(ktab + k0 + (p & 15));
+    }
+  }
+  __device__ __forceinline__ void issue(T* sm, const T* __restrict__ g, int k0, int K, int p) {
+    const int w = p >> 5, l = p & 31;
+    if constexpr (FIXED_VECS) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * w + i;
+        const bool kin = k0 + r < K;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          cp_async_elem(sm + r * LD + l + 32 * j, g + (o[j] + kv[i]), kin && ((valid >> j) & 1u));
+      }
+    } else {
+      const int kk = l & 15;
+      const bool kin = k0 + kk < K;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int r = 32 * w + 2 * q + (l >> 4);
+        cp_async_elem(sm + r * LD + kk, g + (o[q] + kv[0]), kin && ((valid >> q) & 1u));
+      }
+    }
+  }
+};
+
+// Gather mode per operand: 0 = every vector contiguous and aligned (one 16-byte copy each),
+// 1 = per-vector check (16-byte copy where contiguous, element copies elsewhere),
+// 2 = coalesced element copies (GatherElem).
+template <typename T, typename IDX, bool FIXED_VECS, int MODE, int LD> struct GatherSel {
+  using type = Gather<T, IDX, FIXED_VECS, MODE == 0, LD>;
+};
+template <typename T, typename IDX, bool FIXED_VECS, int LD> struct GatherSel<T, IDX, FIXED_VECS, 2, LD> {
+  using type = GatherElem<T, IDX, FIXED_VECS, LD>;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -459,7 +555,7 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
 }
 
-template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC, bool FFMA>
+template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
                   const IDX* __restrict__ rA, const IDX* __restrict__ cA,
@@ -470,12 +566,15 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
                   Sched sched, int* __restrict__ flags) {
   using AL = ALay<T, A_VM>;
   using BL = BLay<T, B_VK>;
+  constexpr int STAGES = stages<T>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
   T* Bs = As + STAGES * AL::STAGE;
   uint64_t* full = reinterpret_cast<uint64_t*>(
       smem_raw + ((STAGES * (AL::STAGE + BL::STAGE) * sizeof(T) + 15) / 16) * 16);
   uint64_t* empty = full + STAGES;
+  // per consumer warp: the C scatter entries of its 64 rows and 32 columns of the current tile
+  IDX* wtab = reinterpret_cast<IDX*>(empty + STAGES) + (threadIdx.x >> 5) * kWarpTab;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -499,20 +598,24 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     // registers move from the producer warpgroup to the two consumer warpgroups
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
     const int p = threadIdx.x - NCW * 32;
-    Gather<T, IDX, A_VM, A_VEC, AL::LD> ga;
-    Gather<T, IDX, !B_VK, B_VEC, BL::LD> gb;
+    typename GatherSel<T, IDX, A_VM, A_MODE, AL::LD>::type ga;
+    typename GatherSel<T, IDX, !B_VK, B_MODE, BL::LD>::type gb;
     while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
       // A's tile bundle is M (rA), B's is N (cB); their K tables are cA and rB.
       ga.init(rA, vA, tm * BM, M, p);
       gb.init(cB, vB, tn * BN, N, p);
+      ga.load_k(cA, vA, kb * BK, K, p);
+      gb.load_k(rB, vB, kb * BK, K, p);
       for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        ga.issue(As + s * AL::STAGE, A, cA, vA, kt * BK, K, p);
-        gb.issue(Bs + s * BL::STAGE, B, rB, vB, kt * BK, K, p);
+        ga.issue(As + s * AL::STAGE, A, kt * BK, K, p);
+        gb.issue(Bs + s * BL::STAGE, B, kt * BK, K, p);
         mbar_cp_async_arrive(&full[s]);
+        ga.load_k(cA, vA, (kt + 1) * BK, K, p);   // next stage's K entries (padded tables)
+        gb.load_k(rB, vB, (kt + 1) * BK, K, p);
       }
     }
     cp_async_wait_all();
@@ -527,6 +630,13 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     int tm, tn;
     tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
     const int m0 = tm * BM, n0 = tn * BN;
+    // fetch this warp's rC / cC entries for the epilogue now (cp.async into its private smem;
+    // tables are padded past M, N), so their latency hides behind the K loop
+    for (int q = lane; q < kWarpTab; q += 32) {
+      const IDX* src = q < WM ? rC + (m0 + mk.wm + q) : cC + (n0 + mk.wn + q - WM);
+      if constexpr (sizeof(IDX) == 8) cp_async8(wtab + q, src, true);
+      else cp_async4(wtab + q, src, true);
+    }
     if (beta != 0.0 && kb == 0 && ke - kb >= 4) {
       // pull the warp's 64 x 32 block of C into L2 while the K loop runs: lane l takes column
       // l and four 16-row runs (one 128-byte line each when C is contiguous along M)
@@ -571,12 +681,14 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     // epilogue: C[rC[m] + cC[n]] = alpha*acc + beta*C (beta == 0: C not read); computed in
     // fp64, rounded once to T. C is read in chunks of 16 independent loads (two of the thread's
     // rows) so the loads of a chunk overlap instead of each waiting behind the previous store.
+    cp_async_wait_all();
+    __syncwarp();
     IDX cc[8];
     int nn[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       nn[c] = n0 + mk.col(c);
-      cc[c] = cC[nn[c]];
+      cc[c] = wtab[WM + mk.col(c) - mk.wn];
     }
     const bool read_c = accumulate || beta != 0.0;
 #pragma unroll
@@ -586,7 +698,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         mm[h] = m0 + mk.row(2 * r2 + h);
-        rc[h] = rC[mm[h]];
+        rc[h] = wtab[mk.row(2 * r2 + h) - mk.wm];
       }
       double old[2][8];
       if (read_c) {
@@ -649,12 +761,13 @@ static Sched make_sched(int T, int KT, int nsm, bool allow_sk) {
   return s;
 }
 
-template <typename T, typename IDX, bool A_VM, bool B_VK, bool A_VEC, bool B_VEC, bool FFMA>
+template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 int launch(const LaunchArgs& a, cudaStream_t stream) {
+  constexpr int STAGES = stages<T>();
   constexpr int smem =
       ((STAGES * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) * (int)sizeof(T) + 15) / 16) * 16 +
-      2 * STAGES * (int)sizeof(uint64_t);
-  auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_VEC, B_VEC, FFMA>;
+      2 * STAGES * (int)sizeof(uint64_t) + NCW * kWarpTab * (int)sizeof(IDX);
+  auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_MODE, B_MODE, FFMA>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -681,23 +794,29 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   return 1;
 }
 
-template <typename T, typename IDX, bool A_VEC, bool B_VEC, bool FFMA>
+template <typename T, typename IDX, int A_MODE, int B_MODE, bool FFMA>
 int dispatch_dir(const LaunchArgs& a, cudaStream_t s) {
   if (a.a_vec_m)
-    return a.b_vec_k ? launch<T, IDX, true, true, A_VEC, B_VEC, FFMA>(a, s)
-                     : launch<T, IDX, true, false, A_VEC, B_VEC, FFMA>(a, s);
-  return a.b_vec_k ? launch<T, IDX, false, true, A_VEC, B_VEC, FFMA>(a, s)
-                   : launch<T, IDX, false, false, A_VEC, B_VEC, FFMA>(a, s);
+    return a.b_vec_k ? launch<T, IDX, true, true, A_MODE, B_MODE, FFMA>(a, s)
+                     : launch<T, IDX, true, false, A_MODE, B_MODE, FFMA>(a, s);
+  return a.b_vec_k ? launch<T, IDX, false, true, A_MODE, B_MODE, FFMA>(a, s)
+                   : launch<T, IDX, false, false, A_MODE, B_MODE, FFMA>(a, s);
 }
 
+// All B gather modes for one A mode (each A mode is instantiated in its own translation unit).
+template <typename T, bool FFMA, int A_MODE>
+int dispatch_b(const LaunchArgs& a, cudaStream_t s) {
+  switch (a.b_mode) {
+    case 0: return dispatch_dir<T, int, A_MODE, 0, FFMA>(a, s);
+    case 1: return dispatch_dir<T, int, A_MODE, 1, FFMA>(a, s);
+    default: return dispatch_dir<T, int, A_MODE, 2, FFMA>(a, s);
+  }
+}
+
+// 64-bit offsets: per-vector gathers only (the element gather keeps 16 offsets per thread).
 template <typename T, bool FFMA>
-int dispatch_type(const LaunchArgs& a, cudaStream_t stream) {
-  if (a.idx64) return dispatch_dir<T, long long, false, false, FFMA>(a, stream);
-  if (a.a_vec_all)
-    return a.b_vec_all ? dispatch_dir<T, int, true, true, FFMA>(a, stream)
-                       : dispatch_dir<T, int, true, false, FFMA>(a, stream);
-  return a.b_vec_all ? dispatch_dir<T, int, false, true, FFMA>(a, stream)
-                     : dispatch_dir<T, int, false, false, FFMA>(a, stream);
+int dispatch_idx64(const LaunchArgs& a, cudaStream_t s) {
+  return dispatch_dir<T, long long, 1, 1, FFMA>(a, s);
 }
 
 }  // namespace ws

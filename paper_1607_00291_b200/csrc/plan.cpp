@@ -258,25 +258,45 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   }
   // GPU traversal order (DESIGN.md §3 R16; "the optimal ordering ... may differ
   // from that achieved by the above heuristics"). The heuristic favours C's unit stride (sort
-  // by C stride) and A's only within P. On the GPU A and B are re-read N/128 and M/128 times
-  // while C is written once, so the kernel walks each bundle with an operand's unit-stride
-  // dimension first: A's (in I or else P), then B's (in P unless A took P's front, or J).
+  // by C stride) and A's only within P. On the GPU the kernel reads A once per N tile and B once
+  // per M tile, while C is written once (a partial-sector write costs about twice a read), so
+  // each bundle is walked with the unit-stride dimension of the tensor that moves the most
+  // elements through it first: in I, A's (weight K*M*ceil(N/128)) against C's (2*M*N); in P,
+  // A's, or B's when A took I; in J, B's (K*N*ceil(M/128)) against C's, when B did not take P.
   // Values are unchanged (same elements, other tile membership); the paper-order tables above
   // stay the plan's reported scatter vectors.
   p->kb = p->b;
-  auto unit_front = [](std::vector<Dim>& d, int w) {
+  auto find_unit = [](const std::vector<Dim>& d, int w) {
     for (size_t i = 0; i < d.size(); ++i)
-      if (d[i].s[w] == 1) {
-        if (i) { Dim x = d[i]; d.erase(d.begin() + (long)i); d.insert(d.begin(), x); }
-        return true;
-      }
-    return false;
+      if (d[i].s[w] == 1) return (int)i;
+    return -1;
   };
-  bool a_m = unit_front(p->kb.I, 0);
+  auto to_front = [](std::vector<Dim>& d, int i) {
+    if (i > 0) { Dim x = d[(size_t)i]; d.erase(d.begin() + i); d.insert(d.begin(), x); }
+  };
+  auto unit_front = [&](std::vector<Dim>& d, int w) {
+    const int i = find_unit(d, w);
+    to_front(d, i);
+    return i >= 0;
+  };
+  const double tiles_n = (double)((p->n + kTileN - 1) / kTileN);
+  const double tiles_m = (double)((p->m + kTileM - 1) / kTileM);
+  const double wA = (double)p->k * (double)p->m * tiles_n;
+  const double wB = (double)p->k * (double)p->n * tiles_m;
+  const double wC = 2.0 * (double)p->m * (double)p->n;
+  bool a_m = false;
+  {
+    const int ia = find_unit(p->kb.I, 0), ic = find_unit(p->kb.I, 1);
+    if (ia >= 0 && (ic < 0 || ic == ia || wA > wC)) { to_front(p->kb.I, ia); a_m = true; }
+    else to_front(p->kb.I, ic);
+  }
   bool a_k = !a_m && unit_front(p->kb.P, 0);
   bool b_k = a_k ? (!p->kb.P.empty() && p->kb.P[0].s[1] == 1) : unit_front(p->kb.P, 1);
-  bool b_n = !b_k && unit_front(p->kb.J, 0);
-  (void)b_n;
+  if (!b_k) {
+    const int jb = find_unit(p->kb.J, 0), jc = find_unit(p->kb.J, 1);
+    if (jb >= 0 && (jc < 0 || jc == jb || wB > wC)) to_front(p->kb.J, jb);
+    else to_front(p->kb.J, jc);
+  }
   if (!p->empty_out) {
     p->kscat[0] = scatter(p->kb.I, 0);
     p->kscat[1] = scatter(p->kb.P, 0);
@@ -302,6 +322,11 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
     p->b_pairs_all = p->b_vec_k ? vec_blocks_all(p->kscat[2], p->kscat[3], V)
                                 : vec_blocks_all(p->kscat[3], p->kscat[2], V);
   }
+  // Gather mode of an operand that is not all-vector (contract_ws.cuh GatherSel), measured on
+  // the cfg4 / f2 suites (profiles/r01/suite_gather_ab.txt): for fp32 the coalesced element
+  // gather wins (a 16-byte vector holds 4 elements, so odd runs misalign most vectors); for fp64
+  // the per-vector check is as good or better (2-element vectors are mostly aligned).
+  p->a_elem = p->b_elem = dtype == TC_F32;
   p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
                (dtype == TC_F32 ? 8 : 0);
   return Status::ok();

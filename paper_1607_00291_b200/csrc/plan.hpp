@@ -52,6 +52,9 @@ bool injective(int rank, const int64_t* lens, const int64_t* strides);
 // [lo, hi] element-offset span of a strided tensor (empty tensors: lo > hi).
 void span(int rank, const int64_t* lens, const int64_t* strides, int64_t* lo, int64_t* hi);
 
+// CTA tile of the contraction kernel (kernels.hpp kBM, kBN), for the traversal-order cost model
+constexpr int64_t kTileM = 128, kTileN = 128;
+
 struct DeviceTables;  // defined in tc_api.cpp
 
 struct Plan {
@@ -70,6 +73,9 @@ struct Plan {
   bool idx64 = false;
   // whole-operand block-scatter check at 16-byte granularity (see vec_blocks_all in plan.cpp)
   bool a_pairs_all = false, b_pairs_all = false;
+  // gather mode for operands that are not all-vector: coalesced element copies (true) or the
+  // per-vector check (false), from the share of vectors that qualify (plan.cpp)
+  bool a_elem = true, b_elem = true;
   int variant = 0;
   // per-device uploaded tables
   mutable std::mutex mu;

@@ -126,6 +126,18 @@ static bool f32_dmma() {
   return f;
 }
 
+// TC_GATHER=mixed|elem forces the gather mode of operands that are not all-vector (ablation);
+// by default the plan decides (Plan::a_elem / b_elem).
+static int gather_override() {
+  static const int g = [] {
+    const char* e = getenv("TC_GATHER");
+    if (e && !strcmp(e, "mixed")) return 1;
+    if (e && !strcmp(e, "elem")) return 2;
+    return 0;
+  }();
+  return g;
+}
+
 static int get_tables(const Plan& p, DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -184,6 +196,8 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
   a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0 && !force_scatter();
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !force_scatter();
+  a.a_elem = gather_override() ? gather_override() == 2 : p.a_elem;
+  a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;
   a.flags = stream_flags(d->device, stream, a.flags_cap);
