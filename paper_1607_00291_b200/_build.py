@@ -19,7 +19,8 @@ OBJ = os.path.join(HERE, "build_obj") if not os.environ.get("TC_LIB_OUT") else L
 EXTRA = os.environ.get("TC_NVCC_EXTRA", "").split()
 SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu",
            "ws_f64_a0.cu", "ws_f64_a1.cu", "ws_f64_a2.cu",
-           "ws_f32_ffma_a0.cu", "ws_f32_ffma_a1.cu", "ws_f32_ffma_a2.cu", "ws_f32_dmma.cu"]
+           "ws_f32_ffma_a0.cu", "ws_f32_ffma_a1.cu", "ws_f32_ffma_a2.cu", "ws_f32_ffma_a3.cu",
+           "ws_f32_dmma.cu"]
 HEADERS = ["plan.hpp", "kernels.hpp", "dev_common.cuh", "contract_ws.cuh"]
 
 NVCC_FLAGS = [

@@ -331,6 +331,7 @@ int launch_ws_f32_ffma_a0(const LaunchArgs& a, cudaStream_t stream);
 int launch_ws_f32_ffma_a1(const LaunchArgs& a, cudaStream_t stream);
 int launch_ws_f32_ffma_a2(const LaunchArgs& a, cudaStream_t stream);
 int launch_ws_f32_ffma_idx64(const LaunchArgs& a, cudaStream_t stream);
+int launch_ws_f32_ffma_a3(const LaunchArgs& a, cudaStream_t stream);
 int launch_ws_f32_dmma(const LaunchArgs& a, cudaStream_t stream);   // ws_f32_dmma.cu
 
 // Gather mode per operand: vectors when the plan proved every vector contiguous and aligned,
@@ -342,6 +343,8 @@ static int launch_ws(const LaunchArgs& args, cudaStream_t stream) {
   if (a.f32 && a.f32_dmma) return launch_ws_f32_dmma(a, stream);
   if (a.idx64) return a.f32 ? launch_ws_f32_ffma_idx64(a, stream) : launch_ws_f64_idx64(a, stream);
   if (a.f32) {
+    // A and B both K-contiguous: transpose A into [k][m] while gathering (TC_FFMA_AT=0: off)
+    if (!a.a_vec_m && a.b_vec_k && a.f32_a_transpose) return launch_ws_f32_ffma_a3(a, stream);
     switch (a.a_mode) {
       case 0: return launch_ws_f32_ffma_a0(a, stream);
       case 1: return launch_ws_f32_ffma_a1(a, stream);

@@ -280,14 +280,57 @@ struct GatherElem {
   }
 };
 
+// Transposing element gather (mode 3, fp32 A only): A is read along K (its unit stride) but
+// written to the [k][m] layout, so that an fp32 contraction whose A and B are both K-contiguous
+// runs the PAIR_R micro-kernel (one accumulator set) instead of PAIR_K (two). Lane l of warp w
+// takes K entry 8 h + (l & 7) and tile row 32 w + 4 g + (l >> 3) (h < 2, g < 8): each warp
+// instruction reads four 32-byte runs and writes 16 distinct banks (2-way conflicts).
+template <typename T, typename IDX, int LD>
+struct GatherElemT {
+  IDX o[8];
+  uint32_t valid;
+  IDX kv[2];
+  __device__ __forceinline__ void init(const IDX* __restrict__ tab, const uint8_t*, int base,
+                                       int extent, int p) {
+    const int w = p >> 5, l = p & 31;
+    valid = 0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const int e = base + 32 * w + 4 * g + (l >> 3);
+      o[g] = tab[e];
+      valid |= (e < extent ? 1u : 0u) << g;
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, const uint8_t*, int k0,
+                                         int, int p) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) kv[h] = __ldg(ktab + k0 + 8 * h + (p & 7));
+  }
+  __device__ __forceinline__ void issue(T* sm, const T* __restrict__ g, int k0, int K, int p) {
+    const int w = p >> 5, l = p & 31;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = 8 * h + (l & 7);
+      const bool kin = k0 + kk < K;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        cp_async_elem(sm + kk * LD + 32 * w + 4 * q + (l >> 3), g + (o[q] + kv[h]),
+                      kin && ((valid >> q) & 1u));
+    }
+  }
+};
+
 // Gather mode per operand: 0 = every vector contiguous and aligned (one 16-byte copy each),
 // 1 = per-vector check (16-byte copy where contiguous, element copies elsewhere),
-// 2 = coalesced element copies (GatherElem).
+// 2 = coalesced element copies (GatherElem), 3 = transposing element copies (GatherElemT).
 template <typename T, typename IDX, bool FIXED_VECS, int MODE, int LD> struct GatherSel {
   using type = Gather<T, IDX, FIXED_VECS, MODE == 0, LD>;
 };
 template <typename T, typename IDX, bool FIXED_VECS, int LD> struct GatherSel<T, IDX, FIXED_VECS, 2, LD> {
   using type = GatherElem<T, IDX, FIXED_VECS, LD>;
+};
+template <typename T, typename IDX, bool FIXED_VECS, int LD> struct GatherSel<T, IDX, FIXED_VECS, 3, LD> {
+  using type = GatherElemT<T, IDX, LD>;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -363,7 +406,10 @@ struct MicroFfma {
   //  PAIR_R: (acc[r][c], acc[r+1][c]) with a[k][r..r+1] ([k][m] layout of A, B is [n][k])
   //  PAIR_K: (acc[r][c], acc2[r][c]) = even / odd k partial sums ([m][k] and [n][k] layouts)
   static constexpr int PAIR_C = 0, PAIR_R = 1, PAIR_K = 2;
-  static constexpr int MODE = !B_VK ? PAIR_C : (A_VM ? PAIR_R : PAIR_K);
+#ifndef TC_FFMA_PAIRK
+#define TC_FFMA_PAIRK 1
+#endif
+  static constexpr int MODE = !B_VK ? PAIR_C : (A_VM ? PAIR_R : (TC_FFMA_PAIRK ? PAIR_K : PAIR_C));
   Acc acc[8][8];
   Acc acc2[MODE == PAIR_K ? 8 : 1][MODE == PAIR_K ? 8 : 1];
   int wm, wn, tm, tn;     // lane = tm + 8 tn (tm 0..7 over M, tn 0..3 over N)
@@ -810,6 +856,17 @@ int dispatch_b(const LaunchArgs& a, cudaStream_t s) {
     case 0: return dispatch_dir<T, int, A_MODE, 0, FFMA>(a, s);
     case 1: return dispatch_dir<T, int, A_MODE, 1, FFMA>(a, s);
     default: return dispatch_dir<T, int, A_MODE, 2, FFMA>(a, s);
+  }
+}
+
+// fp32, A and B both gathered along K: A through the transposing gather (mode 3) into the
+// [k][m] layout, so the consumer runs PAIR_R.
+template <typename T, bool FFMA>
+int dispatch_a_transposed(const LaunchArgs& a, cudaStream_t s) {
+  switch (a.b_mode) {
+    case 0: return launch<T, int, true, true, 3, 0, FFMA>(a, s);
+    case 1: return launch<T, int, true, true, 3, 1, FFMA>(a, s);
+    default: return launch<T, int, true, true, 3, 2, FFMA>(a, s);
   }
 }
 

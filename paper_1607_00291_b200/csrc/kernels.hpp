@@ -32,7 +32,8 @@ struct LaunchArgs {
   // gather mode per operand (contract_ws.cuh GatherSel): 0 vectors, 1 per-vector check,
   // 2 coalesced elements; set by launch_contract from a_vec_all / b_vec_all and the plan
   int a_mode, b_mode;
-  bool a_elem, b_elem;   // the plan prefers the element gather when not all vectors qualify
+  bool a_elem, b_elem;
+  bool f32_a_transpose;  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA

@@ -138,6 +138,14 @@ static int gather_override() {
   return g;
 }
 
+static bool f32_a_transpose() {
+  static const bool f = [] {
+    const char* e = getenv("TC_FFMA_AT");
+    return !(e && !strcmp(e, "0"));
+  }();
+  return f;
+}
+
 static int get_tables(const Plan& p, DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -198,6 +206,7 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !force_scatter();
   a.a_elem = gather_override() ? gather_override() == 2 : p.a_elem;
   a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
+  a.f32_a_transpose = f32_a_transpose() && !force_scatter();
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;
   a.flags = stream_flags(d->device, stream, a.flags_cap);
