@@ -113,7 +113,8 @@ typedef struct {
   int32_t a_vec_m;         /* loader direction for A: 1 = along M (I), 0 = along K (P)       */
   int32_t b_vec_k;         /* loader direction for B: 1 = along K (P), 0 = along N (J)       */
   int32_t idx64;           /* 1 if 64-bit offsets are needed, 0 for 32-bit                   */
-  int32_t variant;         /* kernel variant id                         */
+  int32_t variant;         /* bits: 1 A along M, 2 B along K, 4 int64 offsets, 8 fp32,       */
+                           /* 16 C unit stride along N (epilogue lanes take columns)        */
 } tc_plan_info;
 
 int tc_plan_query(const tc_plan* plan, tc_plan_info* info);

@@ -37,11 +37,12 @@ constexpr int NPT = NPW * 32;               // producer threads
 constexpr int NTHREADS = (NCW + NPW) * 32;
 constexpr int WM = 64, WN = 32;
 constexpr int kWarpTab = WM + WN;           // C scatter entries per consumer warp and tile
-// Ring depth per element type: an fp32 K step computes in half the time of an fp64 one (FFMA
-// at 2x the DMMA rate) and moves half the bytes, so it needs twice the stages in flight to
-// cover the same copy latency.
+// Ring depth per element type. fp32 keeps 4 stages although its K step is twice as short: the
+// element gathers (cp.async 4 B, cached in L1) need the L1 share that a deeper ring plus the
+// epilogue staging buffers would take from the 256 KB L1/shared array (measured: 8 stages cost
+// up to 13% on cfg4 fp32 cases with element-gathered operands, profiles/r01/ab_stages_f32.txt).
 #ifndef TC_STAGES_F32
-#define TC_STAGES_F32 8
+#define TC_STAGES_F32 4
 #endif
 #ifndef TC_STAGES_F64
 #define TC_STAGES_F64 4
@@ -49,6 +50,11 @@ constexpr int kWarpTab = WM + WN;           // C scatter entries per consumer wa
 template <typename T> constexpr int stages() {
   return sizeof(T) == 4 ? TC_STAGES_F32 : TC_STAGES_F64;
 }
+// FFMA epilogue staging (fp32): per consumer warp its 64 x 32 accumulator block as [n][m]
+// floats, row pitch kEpiLD (a multiple of 4 for 16-byte accesses)
+constexpr int kEpiLD = 64 + 4;
+constexpr int kEpiWarpFloats = 32 * kEpiLD;
+constexpr int kSmemLimit = 232448;   // 227 KB of dynamic shared memory per CTA
 constexpr int GROUP_M = 8;
 // setmaxnreg budgets: 128 x 56 + 256 x 224 = 64512 <= 65536 registers per SM, and per SMSP
 // (warps w, w+4, w+8) 224 + 224 + 56 = 504 <= 512 registers per lane.
@@ -601,6 +607,21 @@ __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
 }
 
+// Shared memory: the ring, the full/empty barriers, the per-warp C-table slices and (FFMA) the
+// per-warp epilogue staging buffers; the ring is as deep as stages<T>() allows within 227 KB.
+template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA>
+constexpr int smem_bytes(int stages_) {
+  return ((stages_ * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) * (int)sizeof(T) + 15) / 16) * 16 +
+         2 * stages_ * (int)sizeof(uint64_t) + NCW * kWarpTab * (int)sizeof(IDX) +
+         (FFMA ? NCW * kEpiWarpFloats * (int)sizeof(float) : 0);
+}
+template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA>
+constexpr int ring_stages() {
+  int st = stages<T>();
+  while (st > 2 && smem_bytes<T, A_VM, B_VK, IDX, FFMA>(st) > kSmemLimit) --st;
+  return st;
+}
+
 template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
@@ -609,10 +630,10 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
                   const IDX* __restrict__ rC, const IDX* __restrict__ cC,
                   const uint8_t* __restrict__ vA, const uint8_t* __restrict__ vB,
                   int M, int N, int K, int tiles_m, int tiles_n, double alpha, double beta,
-                  Sched sched, int* __restrict__ flags) {
+                  Sched sched, int* __restrict__ flags, bool c_lanes_n) {
   using AL = ALay<T, A_VM>;
   using BL = BLay<T, B_VK>;
-  constexpr int STAGES = stages<T>();
+  constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
   T* Bs = As + STAGES * AL::STAGE;
@@ -621,6 +642,8 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
   uint64_t* empty = full + STAGES;
   // per consumer warp: the C scatter entries of its 64 rows and 32 columns of the current tile
   IDX* wtab = reinterpret_cast<IDX*>(empty + STAGES) + (threadIdx.x >> 5) * kWarpTab;
+  float* epi = reinterpret_cast<float*>(reinterpret_cast<IDX*>(empty + STAGES) + NCW * kWarpTab) +
+               (threadIdx.x >> 5) * kEpiWarpFloats;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -724,6 +747,94 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     }
     const bool accumulate = split && piece > 0;
 
+    if constexpr (FFMA) {
+      // FFMA epilogue through shared memory: the FFMA micro-kernel's thread layout puts a
+      // lane's rows 4 apart (or 8), so direct stores would touch several times the sectors
+      // they fill. The warp stages its 64 x 32 block as [n][m]; then consecutive lanes write
+      // consecutive elements along C's unit-stride bundle (M: lane l takes rows l and l + 32
+      // of every column; N: lane l takes column l, reading 4 rows per 16-byte load), one
+      // 128-byte run per warp store when that bundle is contiguous. C is read the same way
+      // when beta != 0 or for a stream-K accumulation.
+      __syncwarp();
+      if constexpr (A_VM) {   // rows 4 tm + {0..3} (+ 32): one 16-byte store per column
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          float* d = epi + (mk.col(c) - mk.wn) * kEpiLD + (mk.row(0) - mk.wm);
+          *reinterpret_cast<float4*>(d) =
+              make_float4(mk.value(0, c), mk.value(1, c), mk.value(2, c), mk.value(3, c));
+          *reinterpret_cast<float4*>(d + 32) =
+              make_float4(mk.value(4, c), mk.value(5, c), mk.value(6, c), mk.value(7, c));
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            epi[(mk.col(c) - mk.wn) * kEpiLD + (mk.row(r) - mk.wm)] = mk.value(r, c);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      const bool read_c = accumulate || beta != 0.0;
+      if (!c_lanes_n) {
+        const int ma = m0 + mk.wm + lane, mb = ma + 32;
+        const IDX rca = wtab[lane], rcb = wtab[lane + 32];
+        const bool ina = ma < M, inb = mb < M;
+#pragma unroll 2
+        for (int j0 = 0; j0 < WN; j0 += 8) {
+          float olda[8], oldb[8];
+          IDX cc[8];
+          bool nin[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            cc[j] = wtab[WM + j0 + j];
+            nin[j] = n0 + mk.wn + j0 + j < N;
+            olda[j] = oldb[j] = 0.f;
+            if (read_c) {
+              if (ina && nin[j]) olda[j] = accumulate ? __ldcg(C + (rca + cc[j])) : C[rca + cc[j]];
+              if (inb && nin[j]) oldb[j] = accumulate ? __ldcg(C + (rcb + cc[j])) : C[rcb + cc[j]];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float* src = epi + (j0 + j) * kEpiLD;
+            double va = alpha * static_cast<double>(src[lane]);
+            double vb = alpha * static_cast<double>(src[lane + 32]);
+            if (accumulate) { va += olda[j]; vb += oldb[j]; }
+            else if (beta != 0.0) { va = fma(beta, (double)olda[j], va); vb = fma(beta, (double)oldb[j], vb); }
+            if (ina && nin[j]) C[rca + cc[j]] = static_cast<T>(va);
+            if (inb && nin[j]) C[rcb + cc[j]] = static_cast<T>(vb);
+          }
+        }
+      } else {
+        const int n = n0 + mk.wn + lane;
+        const IDX cc = wtab[WM + lane];
+        const bool nin = n < N;
+#pragma unroll 2
+        for (int i0 = 0; i0 < WM; i0 += 8) {
+          float old[8];
+          IDX rc[8];
+          bool min_[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            rc[i] = wtab[i0 + i];
+            min_[i] = m0 + mk.wm + i0 + i < M;
+            old[i] = 0.f;
+            if (read_c && nin && min_[i]) old[i] = accumulate ? __ldcg(C + (rc[i] + cc)) : C[rc[i] + cc];
+          }
+          const float4 x0 = *reinterpret_cast<const float4*>(epi + lane * kEpiLD + i0);
+          const float4 x1 = *reinterpret_cast<const float4*>(epi + lane * kEpiLD + i0 + 4);
+          const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            double v = alpha * static_cast<double>(xv[i]);
+            if (accumulate) v += old[i];
+            else if (beta != 0.0) v = fma(beta, (double)old[i], v);
+            if (nin && min_[i]) C[rc[i] + cc] = static_cast<T>(v);
+          }
+        }
+      }
+    } else {
+
     // epilogue: C[rC[m] + cC[n]] = alpha*acc + beta*C (beta == 0: C not read); computed in
     // fp64, rounded once to T. C is read in chunks of 16 independent loads (two of the thread's
     // rows) so the loads of a chunk overlap instead of each waiting behind the previous store.
@@ -772,6 +883,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
         }
       }
     }
+    }   // DMMA epilogue
     if (split) {
       // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
       // again when the kernel ends (no per-launch reset)
@@ -809,10 +921,8 @@ static Sched make_sched(int T, int KT, int nsm, bool allow_sk) {
 
 template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 int launch(const LaunchArgs& a, cudaStream_t stream) {
-  constexpr int STAGES = stages<T>();
-  constexpr int smem =
-      ((STAGES * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) * (int)sizeof(T) + 15) / 16) * 16 +
-      2 * STAGES * (int)sizeof(uint64_t) + NCW * kWarpTab * (int)sizeof(IDX);
+  constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
+  constexpr int smem = smem_bytes<T, A_VM, B_VK, IDX, FFMA>(STAGES);
   auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_MODE, B_MODE, FFMA>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -835,7 +945,7 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
       static_cast<const IDX*>(a.rB), static_cast<const IDX*>(a.cB),
       static_cast<const IDX*>(a.rC), static_cast<const IDX*>(a.cC), a.vA, a.vB, a.M, a.N, a.K,
-      tiles_m, tiles_n, a.alpha, a.beta, sc, flags);
+      tiles_m, tiles_n, a.alpha, a.beta, sc, flags, a.c_lanes_n);
   if (cudaPeekAtLastError() != cudaSuccess) return -1;
   return 1;
 }

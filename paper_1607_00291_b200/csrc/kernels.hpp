@@ -33,7 +33,8 @@ struct LaunchArgs {
   // 2 coalesced elements; set by launch_contract from a_vec_all / b_vec_all and the plan
   int a_mode, b_mode;
   bool a_elem, b_elem;
-  bool f32_a_transpose;  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
+  bool f32_a_transpose;
+  bool c_lanes_n;        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA

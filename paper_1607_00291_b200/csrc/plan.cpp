@@ -327,8 +327,16 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   // gather wins (a 16-byte vector holds 4 elements, so odd runs misalign most vectors); for fp64
   // the per-vector check is as good or better (2-element vectors are mostly aligned).
   p->a_elem = p->b_elem = dtype == TC_F32;
+
+  auto unit_steps = [](const std::vector<int64_t>& t) {
+    int64_t u = 0;
+    for (size_t i = 1; i < t.size(); ++i) u += t[i] - t[i - 1] == 1;
+    return (double)u / (double)(t.size() > 1 ? t.size() - 1 : 1);
+  };
+  if (!p->empty_out) p->c_unit_n = unit_steps(p->kscat[5]) > unit_steps(p->kscat[4]);
   p->variant = (p->a_vec_m ? 1 : 0) | (p->b_vec_k ? 2 : 0) | (p->idx64 ? 4 : 0) |
-               (dtype == TC_F32 ? 8 : 0);
+               (dtype == TC_F32 ? 8 : 0) |
+               (p->c_unit_n ? 16 : 0);
   return Status::ok();
 }
 

@@ -76,6 +76,8 @@ struct Plan {
   // gather mode for operands that are not all-vector: coalesced element copies (true) or the
   // per-vector check (false), from the share of vectors that qualify (plan.cpp)
   bool a_elem = true, b_elem = true;
+  // C's traversal tables: more unit steps along N (cscat_C) than along M (rscat_C)
+  bool c_unit_n = false;
   int variant = 0;
   // per-device uploaded tables
   mutable std::mutex mu;
