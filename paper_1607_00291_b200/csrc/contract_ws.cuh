@@ -55,7 +55,16 @@ template <typename T> constexpr int stages() {
 constexpr int kEpiLD = 64 + 4;
 constexpr int kEpiWarpFloats = 32 * kEpiLD;
 constexpr int kSmemLimit = 232448;   // 227 KB of dynamic shared memory per CTA
-constexpr int GROUP_M = 8;
+// Tile rasterisation group height. With K in the tens of thousands a CTA's A and B panels are
+// tens of MB, and the CTAs of a wave drift apart in K faster than L2 (126 MB, turned over every
+// ~80 us at cfg5's miss rate) can bridge, so sharing within a wave is small; what L2 does keep
+// is the A panels of the few tile rows that consecutive waves revisit. Two rows per group keep
+// those resident: cfg5 DRAM reads 3.82 TB (8 rows) -> 3.02 TB per launch, same time
+// (profiles/r01/l2_group_sweep_cfg5.txt); neutral on every other suite case.
+#ifndef TC_GROUP_M
+#define TC_GROUP_M 2
+#endif
+constexpr int GROUP_M = TC_GROUP_M;
 // setmaxnreg budgets: 128 x 56 + 256 x 224 = 64512 <= 65536 registers per SM, and per SMSP
 // (warps w, w+4, w+8) 224 + 224 + 56 = 504 <= 512 registers per lane.
 constexpr int kProducerRegs = 64;
@@ -562,6 +571,12 @@ struct Sched {
   int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
   int P_sk;                 // CTAs in the stream-K tail (0: no tail)
   long long I;              // stream-K iterations = (T - D) * KT
+  // wave alignment of the data-parallel phase: before its j-th whole tile (j >= 1) a CTA's
+  // producers wait (bounded) until the wave counter reaches wave_base + j * P, i.e. every CTA
+  // has issued its loads of wave j - 1, so the CTAs of a wave walk K together and share the A
+  // and B panels in L2 instead of drifting apart over hundreds of waves
+  unsigned wave_base;
+  int wave_sync;
 };
 
 struct WorkIter {
@@ -602,6 +617,22 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void producers_sync() {
+  asm volatile("bar.sync 2, %0;\n" ::"n"(NPT) : "memory");
+}
+// Bounded wait (about 20 us) for the wave counter: a CTA that is not co-resident with the rest
+// of the grid can only delay the others, never deadlock them.
+constexpr long long kWaveTimeout = 40000;
+__device__ __forceinline__ void wave_wait(const int* ctr, unsigned target) {
+  const long long t0 = clock64();
+  while ((int)((unsigned)ld_acquire(ctr) - target) < 0) {
+    if (clock64() - t0 > kWaveTimeout) break;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void wave_arrive(int* ctr) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(ctr) : "memory");
 }
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;\n" ::"n"(NCW * 32) : "memory");
@@ -669,7 +700,13 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     const int p = threadIdx.x - NCW * 32;
     typename GatherSel<T, IDX, A_VM, A_MODE, AL::LD>::type ga;
     typename GatherSel<T, IDX, !B_VK, B_MODE, BL::LD>::type gb;
+    int* wave_ctr = flags + 2 * sched.P;   // after the stream-K flags
+    int dp_items = 0;
     while (wi.next(tile, kb, ke, sk)) {
+      if (!sk && sched.wave_sync && dp_items > 0) {
+        if (p == 0) wave_wait(wave_ctr, sched.wave_base + (unsigned)(dp_items * sched.P));
+        producers_sync();
+      }
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
       // A's tile bundle is M (rA), B's is N (cB); their K tables are cA and rB.
@@ -685,6 +722,10 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
         mbar_cp_async_arrive(&full[s]);
         ga.load_k(cA, vA, (kt + 1) * BK, K, p);   // next stage's K entries (padded tables)
         gb.load_k(rB, vB, (kt + 1) * BK, K, p);
+      }
+      if (!sk && sched.wave_sync) {
+        if (p == 0) wave_arrive(wave_ctr);
+        ++dp_items;
       }
     }
     cp_async_wait_all();
@@ -940,6 +981,11 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   }
   int* flags = a.flags;
   const int grid = sc.D > 0 ? sc.P : sc.P_sk;
+  sc.wave_sync = a.wave_sync && a.wave_base != nullptr && sc.D >= 2 * sc.P;
+  if (sc.wave_sync) {
+    sc.wave_base = *a.wave_base;
+    *a.wave_base += (unsigned)sc.D;   // every whole tile adds one to the counter
+  }
   kern<<<grid, NTHREADS, smem, stream>>>(
       static_cast<const T*>(a.A), static_cast<const T*>(a.B), static_cast<T*>(a.C),
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),

@@ -39,7 +39,9 @@ struct LaunchArgs {
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA
   int* flags;         // stream-K fix-up flags: >= flags_cap zeroed ints, private to the stream
-  int flags_cap;
+  int flags_cap;      // flags[flags_cap] is the wave counter (monotonic, see Sched)
+  unsigned* wave_base;   // host copy of the wave counter's value for this stream
+  bool wave_sync;
 };
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).

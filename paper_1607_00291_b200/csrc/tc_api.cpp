@@ -56,18 +56,34 @@ struct FlagKey {
     return device != o.device ? device < o.device : stream < o.stream;
   }
 };
+// After the flags, one int is the wave counter of the data-parallel phase: it only grows (each
+// whole tile adds 1) and the host keeps its expected value per stream (`wave_base`).
+struct StreamFlags {
+  int* flags = nullptr;
+  unsigned wave_base = 0;
+};
 static std::mutex g_flags_mu;
-static std::map<FlagKey, int*> g_flags;
+static std::map<FlagKey, StreamFlags> g_flags;
 
-static int* stream_flags(int device, cudaStream_t s, int cap) {
+static StreamFlags* stream_flags(int device, cudaStream_t s, int cap) {
   std::lock_guard<std::mutex> lk(g_flags_mu);
   auto it = g_flags.find({device, s});
-  if (it != g_flags.end()) return it->second;
+  if (it != g_flags.end()) return &it->second;
   int* f = nullptr;
-  if (cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int) * (size_t)cap) != cudaSuccess)
+  if (cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int) * (size_t)(cap + 1)) != cudaSuccess)
     return nullptr;
-  if (cudaMemset(f, 0, sizeof(int) * (size_t)cap) != cudaSuccess) { cudaFree(f); return nullptr; }
-  g_flags[{device, s}] = f;
+  if (cudaMemset(f, 0, sizeof(int) * (size_t)(cap + 1)) != cudaSuccess) { cudaFree(f); return nullptr; }
+  StreamFlags& sf = g_flags[{device, s}];
+  sf.flags = f;
+  return &sf;
+}
+
+// TC_WAVE_SYNC=0 turns off the wave alignment of the data-parallel phase (ablation).
+static bool wave_sync() {
+  static const bool f = [] {
+    const char* e = getenv("TC_WAVE_SYNC");
+    return !(e && !strcmp(e, "0"));
+  }();
   return f;
 }
 
@@ -210,7 +226,10 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.c_lanes_n = p.c_unit_n;
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;
-  a.flags = stream_flags(d->device, stream, a.flags_cap);
+  StreamFlags* sf = stream_flags(d->device, stream, a.flags_cap);
+  a.flags = sf ? sf->flags : nullptr;
+  a.wave_base = sf ? &sf->wave_base : nullptr;
+  a.wave_sync = sf != nullptr && wave_sync();
   a.stream_k = a.flags != nullptr;
   a.f32_dmma = f32_dmma();
   if (a.K == 0) { a.A = a.C; a.B = a.C; }  // never dereferenced
