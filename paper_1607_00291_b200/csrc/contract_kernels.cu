@@ -371,9 +371,21 @@ static int kernel_choice() {
   return choice;
 }
 
+// The skinny-contraction kernel (skinny.cu) is opt-in while it is slower than the general
+// kernel on most skinny cases (profiles/r01/suite_f2_skinny_ab.txt): TC_SKINNY=1 enables it.
+// Read on every call, so tests can switch it.
+static bool skinny_enabled() {
+  const char* e = getenv("TC_SKINNY");
+  return e && !strcmp(e, "1");
+}
+
 int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (args.M <= 0 || args.N <= 0) return 0;
   const int choice = kernel_choice();
+  if (choice == 0 && skinny_enabled()) {
+    const int r = launch_skinny(args, stream);
+    if (r != 0) return r;
+  }
   if (choice == 1 && !args.f32)
     return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
   LaunchArgs a = args;

@@ -44,6 +44,10 @@ struct LaunchArgs {
   bool wave_sync;
 };
 
+// Skinny contractions (fp64, K <= 80, one free extent <= 96, the other >= 4096): skinny.cu.
+// 0 = not applicable, 1 = launched, -1 = CUDA error.
+int launch_skinny(const LaunchArgs& a, cudaStream_t stream);
+
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
 int launch_contract(const LaunchArgs& a, cudaStream_t stream);
 

@@ -1,0 +1,246 @@
+// Skinny-contraction kernel (sm_100a, fp64): one free bundle and the bound bundle are small
+// (extent <= 96 and <= 80), the other free bundle is long -- e.g. fig:bench's abcde-efbad-cf
+// with M ~ 1e6, N = K = 32. Such a contraction is an HBM stream: the long operand X
+// (M x K) is read once and C (M x N) is written once, while the small operand Y (K x N) stays
+// in shared memory for the whole kernel. The general 128 x 128 tile would spend most of its
+// DMMA work on padding and restart its pipeline every 2-5 K steps.
+//
+// Persistent CTAs (one per SM, 256 threads) each load Y once (gathered through its scatter
+// vectors), then walk 64-row blocks of X: a 3-deep ring of X blocks is gathered
+// with cp.async (coalesced element copies along X's unit-stride direction, written to the
+// [k][row] layout), each block is multiplied on the FP64 tensor cores (mma.sync m16n8k4 f64 ->
+// DMMA.8x8x4; 8 warps = 4 row groups x 2 column halves) and written through the scatter
+// vectors of C with alpha / beta (beta == 0 never reads C).
+//
+// Roles: X = A (rows = I, tables rA / cA), Y = B (cB / rB) when the small free bundle is J;
+// X = B, Y = A (the transposed problem C^T = B^T A^T) when it is I.
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "dev_common.cuh"
+#include "kernels.hpp"
+
+namespace tcb {
+namespace skinny {
+
+using namespace dev;
+
+constexpr int kRows = 64;           // X rows per block
+constexpr int kThreads = 256;
+constexpr int kMaxN = 96;           // small free extent (padded to a multiple of 16)
+constexpr int kMaxK = 80;           // bound extent (padded to a multiple of 4)
+constexpr int kBufs = 3;            // X ring depth
+constexpr int kXP = kRows + 4;      // [k][row] pitch (doubles): conflict-free fragment loads
+
+struct Args {
+  const double* X;
+  const double* Y;
+  double* C;
+  const void* xr;   // X row table (long bundle)
+  const void* xk;   // X K table
+  const void* yk;   // Y K table
+  const void* yc;   // Y column table (small bundle)
+  const void* cr;   // C offsets along the long bundle
+  const void* cc;   // C offsets along the small bundle
+  int R, NC, K;     // long extent, small extent, bound extent
+  int NP, KP;       // NC rounded up to 16, K rounded up to 4
+  double alpha, beta;
+};
+
+template <typename IDX, int NW>   // NW: n8 blocks per warp (NP / 16)
+__device__ __forceinline__ void block_mma(const double* xs, const double* ys, int yp, int KP,
+                                          int wr, int wc, int g, int t, double (&acc)[NW][4]) {
+#pragma unroll
+  for (int j = 0; j < NW; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[j][q] = 0.0;
+  // fragments of step k4 + 4 load while step k4 multiplies (KP is a multiple of 4)
+  double a0 = xs[t * kXP + wr + g], a1 = xs[t * kXP + wr + g + 8], b[NW];
+#pragma unroll
+  for (int j = 0; j < NW; ++j) b[j] = ys[t * yp + wc + 8 * j + g];
+  for (int k4 = 0; k4 < KP; k4 += 4) {
+    const int kn = k4 + 4 < KP ? k4 + 4 : k4;
+    const double na0 = xs[(kn + t) * kXP + wr + g], na1 = xs[(kn + t) * kXP + wr + g + 8];
+    double nb[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) nb[j] = ys[(kn + t) * yp + wc + 8 * j + g];
+#pragma unroll
+    for (int j = 0; j < NW; ++j)
+      dmma16x8x4(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, b[j]);
+    a0 = na0; a1 = na1;
+#pragma unroll
+    for (int j = 0; j < NW; ++j) b[j] = nb[j];
+  }
+}
+
+// ROWS_UNIT: X is contiguous along its rows (lanes take consecutive rows); otherwise along K
+// (lanes take 8 consecutive K entries of 4 rows).
+template <typename IDX, bool ROWS_UNIT, int NW>
+__global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int yp = a.NP + 4;   // [k][col] pitch of Y (doubles), = 8 (mod 16) words per row
+  double* ys = reinterpret_cast<double*>(smem_raw);
+  double* xs = ys + a.KP * yp;
+  const IDX* xr = static_cast<const IDX*>(a.xr);
+  const IDX* xk = static_cast<const IDX*>(a.xk);
+  const IDX* yk = static_cast<const IDX*>(a.yk);
+  const IDX* yc = static_cast<const IDX*>(a.yc);
+  const IDX* cr = static_cast<const IDX*>(a.cr);
+  const IDX* cc = static_cast<const IDX*>(a.cc);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // Y, once per CTA (zero-filled outside K x NC)
+  for (int e = tid; e < a.KP * a.NP; e += kThreads) {
+    const int k = e / a.NP, n = e - k * a.NP;
+    const bool in = k < a.K && n < a.NC;
+    cp_async8(ys + k * yp + n, a.Y + (in ? yk[k] + yc[n] : 0), in);
+  }
+  cp_async_commit();
+
+  const int nblk = (a.R + kRows - 1) / kRows;
+  auto load_x = [&](int blk, int buf) {
+    double* d = xs + buf * (a.KP * kXP);
+    const int r0 = blk * kRows;
+    if constexpr (ROWS_UNIT) {
+      // lanes: 32 consecutive rows; warps and passes cover the K entries
+      for (int k = warp; k < a.KP; k += kThreads / 32) {
+        const bool kin = k < a.K;
+        const IDX ko = kin ? xk[k] : 0;
+#pragma unroll
+        for (int h = 0; h < kRows / 32; ++h) {
+          const int r = r0 + 32 * h + lane;
+          const bool in = kin && r < a.R;
+          cp_async8(d + k * kXP + 32 * h + lane, a.X + (in ? xr[r] + ko : 0), in);
+        }
+      }
+    } else {
+      // lanes: 8 consecutive K entries x 4 rows
+      const int kk = lane & 7, rr = lane >> 3;
+      for (int rb = 4 * warp; rb < kRows; rb += 4 * (kThreads / 32)) {
+        const int r = r0 + rb + rr;
+        const bool rin = r < a.R;
+        const IDX ro = rin ? xr[r] : 0;
+        for (int k0 = 0; k0 < a.KP; k0 += 8) {
+          const int k = k0 + kk;
+          if (k < a.KP) {
+            const bool in = rin && k < a.K;
+            cp_async8(d + k * kXP + rb + rr, a.X + (in ? ro + xk[k] : 0), in);
+          }
+        }
+      }
+    }
+  };
+
+  // ring of kBufs X blocks: blocks blockIdx.x + i * gridDim.x
+  int issued = 0;
+  for (int i = 0; i < kBufs - 1; ++i) {
+    const int blk = blockIdx.x + i * gridDim.x;
+    if (blk < nblk) load_x(blk, i);
+    cp_async_commit();
+    ++issued;
+  }
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = 16 * (warp & 3), wc = (warp >> 2) * (a.NP / 2);
+  double acc[NW][4];
+  for (int it = 0;; ++it) {
+    const int blk = blockIdx.x + it * gridDim.x;
+    if (blk >= nblk) break;
+    {   // keep kBufs - 1 blocks in flight
+      const int nb = blockIdx.x + (it + kBufs - 1) * gridDim.x;
+      if (nb < nblk) load_x(nb, (it + kBufs - 1) % kBufs);
+      cp_async_commit();
+    }
+    cp_async_wait<kBufs - 1>();
+    __syncthreads();
+    block_mma<IDX, NW>(xs + (it % kBufs) * (a.KP * kXP), ys, yp, a.KP, wr, wc, g, t, acc);
+    // epilogue: rows wr + g (+8), columns wc + 8 j + 2 t (+1)
+    const int r0 = blk * kRows + wr + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + 8 * h;
+      if (r >= a.R) continue;
+      const IDX ro = cr[r];
+#pragma unroll
+      for (int j = 0; j < NW; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = wc + 8 * j + 2 * t + e;
+          if (n >= a.NC) continue;
+          double* q = a.C + (ro + cc[n]);
+          double v = a.alpha * acc[j][2 * h + e];
+          if (a.beta != 0.0) v = fma(a.beta, *q, v);
+          *q = v;
+        }
+    }
+    __syncthreads();   // the buffer of block `it` is refilled at iteration it + 1
+  }
+  cp_async_wait_all();
+}
+
+template <typename IDX, bool ROWS_UNIT, int NW>
+static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
+  const int smem = (a.KP * (a.NP + 4) + kBufs * a.KP * kXP) * (int)sizeof(double);
+  auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW>;
+  static int attr = 0;
+  if (attr < smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return -1;
+    attr = smem;
+  }
+  const int nblk = (a.R + kRows - 1) / kRows;
+  const int grid = nblk < nsm ? nblk : nsm;
+  kern<<<grid, kThreads, smem, s>>>(a);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename IDX, bool ROWS_UNIT>
+static int launch_dir(const Args& a, int nsm, cudaStream_t s) {
+  switch (a.NP / 16) {
+    case 1: return launch_nw<IDX, ROWS_UNIT, 1>(a, nsm, s);
+    case 2: return launch_nw<IDX, ROWS_UNIT, 2>(a, nsm, s);
+    case 3: return launch_nw<IDX, ROWS_UNIT, 3>(a, nsm, s);
+    case 4: return launch_nw<IDX, ROWS_UNIT, 4>(a, nsm, s);
+    case 5: return launch_nw<IDX, ROWS_UNIT, 5>(a, nsm, s);
+    default: return launch_nw<IDX, ROWS_UNIT, 6>(a, nsm, s);
+  }
+}
+
+}  // namespace skinny
+
+// The skinny path applies to fp64 contractions with K <= 80 and one free extent <= 96 (the
+// small extent becomes the resident operand's columns). Returns 0 when it does not apply,
+// 1 on launch, -1 on a CUDA error.
+int launch_skinny(const LaunchArgs& la, cudaStream_t stream) {
+  using namespace skinny;
+  if (la.f32 || la.K < 1 || la.K > kMaxK) return 0;
+  const bool small_n = la.N <= kMaxN;
+  const bool small_m = !small_n && la.M <= kMaxN;
+  if (!small_n && !small_m) return 0;
+  Args a{};
+  bool rows_unit;
+  if (small_n) {   // X = A (rows M), Y = B
+    a.X = static_cast<const double*>(la.A); a.Y = static_cast<const double*>(la.B);
+    a.xr = la.rA; a.xk = la.cA; a.yk = la.rB; a.yc = la.cB; a.cr = la.rC; a.cc = la.cC;
+    a.R = la.M; a.NC = la.N;
+    rows_unit = la.a_vec_m;
+  } else {         // X = B (rows N), Y = A: C^T = B^T A^T
+    a.X = static_cast<const double*>(la.B); a.Y = static_cast<const double*>(la.A);
+    a.xr = la.cB; a.xk = la.rB; a.yk = la.cA; a.yc = la.rA; a.cr = la.cC; a.cc = la.rC;
+    a.R = la.N; a.NC = la.M;
+    rows_unit = !la.b_vec_k;
+  }
+  a.C = static_cast<double*>(la.C);
+  a.K = la.K;
+  a.NP = (a.NC + 15) / 16 * 16;
+  a.KP = (a.K + 3) / 4 * 4;
+  a.alpha = la.alpha; a.beta = la.beta;
+  if (la.idx64)
+    return rows_unit ? launch_dir<long long, true>(a, la.num_sms, stream)
+                     : launch_dir<long long, false>(a, la.num_sms, stream);
+  return rows_unit ? launch_dir<int, true>(a, la.num_sms, stream)
+                   : launch_dir<int, false>(a, la.num_sms, stream);
+}
+
+}  // namespace tcb

@@ -543,3 +543,27 @@ def test_guard_bands(seed, dtype):
     got = Cd.cpu()
     assert torch.isfinite(got).all() or not torch.isfinite(ref).all(), "read outside A/B"
     assert relerr(got.numpy(), ref.numpy()) <= TOL[dtype]
+
+
+# ---------------------------------------------------------------------------------------------
+# skinny contractions (skinny.cu: fp64, K <= 80, one free extent <= 96, the other >= 4096)
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("spec,lens,beta", [
+    ("mn-mk-kn", {"m": 5000, "n": 37, "k": 29}, 0.5),      # X = A along its rows
+    ("mn-km-kn", {"m": 4100, "n": 96, "k": 80}, 0.0),      # X = A along K (transposing gather)
+    ("mn-mk-kn", {"m": 50, "n": 6000, "k": 13}, -1.0),     # small M: X = B, along K
+    ("mn-mk-nk", {"m": 64, "n": 4097, "k": 80}, 0.0),      # small M: X = B along its rows
+    ("mn-mk-kn", {"m": 4096, "n": 1, "k": 1}, 1.0),        # degenerate N = K = 1
+    ("abcde-efbad-cf", {"a": 9, "b": 9, "c": 19, "d": 9, "e": 9, "f": 23}, 0.0),  # fig:bench 0
+])
+@pytest.mark.parametrize("skinny", ["1", "0"])
+def test_skinny_shapes(spec, lens, beta, skinny, monkeypatch):
+    monkeypatch.setenv("TC_SKINNY", skinny)   # the library reads it on every call
+    lc, la, lb = spec.split("-")
+    case = W.Case("skinny_" + spec, lc, la, lb, lens, alpha=0.75, beta=beta,
+                  c_init="dist" if beta else "nan", seed=31)
+    check(case)
+    case.dist, case.alpha = "int", 2.0
+    case.beta = 0.5 if beta else 0.0
+    check(case, bitwise=True)
