@@ -139,7 +139,7 @@ def _desc(t, labels: str, role: int = 0) -> Desc:
 def _stream_ptr(stream) -> Optional[int]:
     import torch
     if stream is None:
-        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     return stream.cuda_stream
 
 

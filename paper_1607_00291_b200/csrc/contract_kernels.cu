@@ -379,9 +379,19 @@ static bool skinny_enabled() {
   return e && !strcmp(e, "1");
 }
 
+// TC_TINY=0 sends tiny contractions to the tensor-core kernel too (tests cover both paths).
+static bool tiny_enabled() {
+  const char* e = getenv("TC_TINY");
+  return !(e && !strcmp(e, "0"));
+}
+
 int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (args.M <= 0 || args.N <= 0) return 0;
   const int choice = kernel_choice();
+  if (choice == 0 && tiny_enabled()) {
+    const int r = launch_tiny(args, stream);
+    if (r != 0) return r;
+  }
   if (choice == 0 && skinny_enabled()) {
     const int r = launch_skinny(args, stream);
     if (r != 0) return r;

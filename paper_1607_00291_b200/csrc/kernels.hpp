@@ -48,6 +48,10 @@ struct LaunchArgs {
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_skinny(const LaunchArgs& a, cudaStream_t stream);
 
+// Tiny contractions (<= 2^21 multiply-adds, <= 2^16 elements of C): tiny.cu, one thread per
+// element of C. 0 = not applicable, 1 = launched, -1 = CUDA error.
+int launch_tiny(const LaunchArgs& a, cudaStream_t stream);
+
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
 int launch_contract(const LaunchArgs& a, cudaStream_t stream);
 

@@ -31,6 +31,14 @@ def tc():
     return m
 
 
+@pytest.fixture(params=["1", "0"], ids=["tiny", "tensorcore"])
+def both_small_paths(request, monkeypatch):
+    """Small cases run through the tiny kernel (tiny.cu) and, with TC_TINY=0, through the
+    tensor-core kernel; the library reads TC_TINY on every call."""
+    monkeypatch.setenv("TC_TINY", request.param)
+    return request.param
+
+
 def relerr(got, ref):
     got = np.asarray(got, dtype=np.float64).ravel()
     ref = np.asarray(ref, dtype=np.float64).ravel()
@@ -89,11 +97,13 @@ def sampled_check(case, Ad, Bd, Cd_before, Cd_after, per_label=3, seed=0):
 # BASELINE configs (small enough for the full oracle, or scaled with ragged tails)
 # ---------------------------------------------------------------------------------------------
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_cfg1_full_nan_C_beta0():
     got, _ = check(W.cfg1())
     assert torch.isfinite(got).all()
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_cfg1_integer_bitwise():
     case = W.cfg1()
     case.dist = "int"
@@ -193,17 +203,20 @@ def test_all_loader_direction_combinations(spec):
     check(case, bitwise=True)
 
 
+@pytest.mark.usefixtures("both_small_paths")
 @pytest.mark.parametrize("seed", range(30))
 def test_random_small_contractions(seed):
     case = W.random_tiny_case(seed, max_rank=6, max_len=7)
     check(case)
 
 
+@pytest.mark.usefixtures("both_small_paths")
 @pytest.mark.parametrize("seed", range(10))
 def test_random_small_integer_bitwise(seed):
     check(W.random_tiny_case(seed, max_rank=6, max_len=7, dist="int"), bitwise=True)
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_alpha_zero_does_not_read_A_B():
     case = W.cfg3(False, v=8, o=4)
     Ad, Bd, Cd = W.make_tensors(case, "cuda")
@@ -213,6 +226,7 @@ def test_alpha_zero_does_not_read_A_B():
     assert torch.equal(Cd, 0.5 * C0)
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_zero_length_and_empty_bundles():
     dev = "cuda"
     A = torch.randn(5, 0, dtype=torch.float64, device=dev)
@@ -235,6 +249,7 @@ def test_zero_length_and_empty_bundles():
         assert relerr(Cd.cpu().numpy(), ref.numpy()) < 1e-13, spec
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_strided_subviews_and_misaligned_bases():
     """Sub-views with gaps and odd element offsets (16-byte vectors disabled per element)."""
     rs = torch.Generator().manual_seed(3)
@@ -259,6 +274,7 @@ def test_strided_subviews_and_misaligned_bases():
         assert torch.equal(bigCd.cpu()[mask], bigC[mask])
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_storage_permutation_invariance_bitwise():
     """Permuting an operand's storage with its labels gives identical C (pin p3(i), int mode)."""
     base = W.Case("perm", "abij", "abef", "efij", {"a": 20, "b": 11, "e": 9, "f": 13, "i": 6, "j": 7},
@@ -401,11 +417,13 @@ def test_f32_loader_directions(spec, mnk):
     check(case, bitwise=True)
 
 
+@pytest.mark.usefixtures("both_small_paths")
 @pytest.mark.parametrize("seed", range(15))
 def test_random_small_f32(seed):
     check(W.random_tiny_case(seed, max_rank=6, max_len=7, dtype=torch.float32))
 
 
+@pytest.mark.usefixtures("both_small_paths")
 def test_f32_misaligned_views():
     g = torch.Generator().manual_seed(4)
     bigA = torch.rand(70, 9, 61, generator=g)
@@ -519,6 +537,7 @@ def _embed(t, device, fill, rs, gap):
     return buf, view
 
 
+@pytest.mark.usefixtures("both_small_paths")
 @pytest.mark.parametrize("seed", range(24))
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 def test_guard_bands(seed, dtype):
