@@ -946,8 +946,13 @@ constexpr int kMaxPieces = 16;   // at most this many stream-K pieces per tile (
 static Sched make_sched(int T, int KT, int nsm, bool allow_sk) {
   Sched s{};
   s.T = T; s.KT = KT; s.P = nsm;
+  // Which tiles are split: the last full wave and the partial wave (stream-K over 1-2 waves,
+  // enough iterations per CTA for a short tail), unless the partial wave is >= 88% full, which
+  // then runs data-parallel (its idle share is smaller than the cost of the split pieces'
+  // extra epilogues). Measured on cfg4 (profiles/r01/ab_sk_policy.txt).
   int D;
-  if (!allow_sk || KT == 0 || T % nsm == 0) D = T;
+  const int rem = T % nsm;
+  if (!allow_sk || KT == 0 || rem == 0 || rem * 100 >= 88 * nsm) D = T;
   else if (T < nsm) D = 0;
   else D = (T / nsm - 1) * nsm;
   s.D = D;
