@@ -371,12 +371,15 @@ static int kernel_choice() {
   return choice;
 }
 
-// The skinny-contraction kernel (skinny.cu) is opt-in while it is slower than the general
-// kernel on most skinny cases (profiles/r01/suite_f2_skinny_ab.txt): TC_SKINNY=1 enables it.
-// Read on every call, so tests can switch it.
-static bool skinny_enabled() {
+// The skinny-contraction kernel (skinny.cu) runs by default when its streamed operand is
+// contiguous along the long bundle (there it beats the tensor-core tile: f2 abcd-ebad-ce 0.82 ->
+// 0.99 of DGEMM, profiles/r01/suite_f2_skinny_ab.txt); TC_SKINNY=1 forces it for every skinny
+// shape, TC_SKINNY=0 turns it off. Read on every call, so tests can switch it.
+static int skinny_mode() {
   const char* e = getenv("TC_SKINNY");
-  return e && !strcmp(e, "1");
+  if (e && !strcmp(e, "1")) return 2;
+  if (e && !strcmp(e, "0")) return 0;
+  return 1;
 }
 
 // TC_TINY=0 sends tiny contractions to the tensor-core kernel too (tests cover both paths).
@@ -392,8 +395,8 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
     const int r = launch_tiny(args, stream);
     if (r != 0) return r;
   }
-  if (choice == 0 && skinny_enabled()) {
-    const int r = launch_skinny(args, stream);
+  if (choice == 0 && skinny_mode() != 0) {
+    const int r = launch_skinny(args, stream, skinny_mode() == 2);
     if (r != 0) return r;
   }
   if (choice == 1 && !args.f32)

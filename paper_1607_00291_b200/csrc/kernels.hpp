@@ -44,9 +44,10 @@ struct LaunchArgs {
   bool wave_sync;
 };
 
-// Skinny contractions (fp64, K <= 80, one free extent <= 96, the other >= 4096): skinny.cu.
+// Skinny contractions (fp64, K <= 80, one free extent <= 96): skinny.cu.
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
-int launch_skinny(const LaunchArgs& a, cudaStream_t stream);
+// `force`: also when the streamed operand is not contiguous along its rows.
+int launch_skinny(const LaunchArgs& a, cudaStream_t stream, bool force);
 
 // Tiny contractions (<= 2^21 multiply-adds, <= 2^16 elements of C): tiny.cu, one thread per
 // element of C. 0 = not applicable, 1 = launched, -1 = CUDA error.

@@ -82,6 +82,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   const int yp = a.NP + 4;   // [k][col] pitch of Y (doubles), = 8 (mod 16) words per row
   double* ys = reinterpret_cast<double*>(smem_raw);
   double* xs = ys + a.KP * yp;
+  // X's K offsets and C's small-bundle offsets, once per CTA (read from shared memory by the
+  // loader and the epilogue instead of a dependent global load per copy / store)
+  IDX* xks = reinterpret_cast<IDX*>(xs + kBufs * a.KP * kXP);
+  IDX* ccs = xks + a.KP;
   const IDX* xr = static_cast<const IDX*>(a.xr);
   const IDX* xk = static_cast<const IDX*>(a.xk);
   const IDX* yk = static_cast<const IDX*>(a.yk);
@@ -90,6 +94,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   const IDX* cc = static_cast<const IDX*>(a.cc);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+  for (int k = tid; k < a.KP; k += kThreads) xks[k] = k < a.K ? xk[k] : 0;
+  for (int n = tid; n < a.NP; n += kThreads) ccs[n] = n < a.NC ? cc[n] : 0;
+  __syncthreads();
   // Y, once per CTA (zero-filled outside K x NC)
   for (int e = tid; e < a.KP * a.NP; e += kThreads) {
     const int k = e / a.NP, n = e - k * a.NP;
@@ -103,30 +110,42 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
     double* d = xs + buf * (a.KP * kXP);
     const int r0 = blk * kRows;
     if constexpr (ROWS_UNIT) {
-      // lanes: 32 consecutive rows; warps and passes cover the K entries
+      // lanes: 32 consecutive rows (two row offsets per lane); warps stride over K
+      IDX ro[kRows / 32];
+      bool rin[kRows / 32];
+#pragma unroll
+      for (int h = 0; h < kRows / 32; ++h) {
+        const int r = r0 + 32 * h + lane;
+        rin[h] = r < a.R;
+        ro[h] = rin[h] ? xr[r] : 0;
+      }
+#pragma unroll 4
       for (int k = warp; k < a.KP; k += kThreads / 32) {
         const bool kin = k < a.K;
-        const IDX ko = kin ? xk[k] : 0;
+        const IDX ko = xks[k];
 #pragma unroll
-        for (int h = 0; h < kRows / 32; ++h) {
-          const int r = r0 + 32 * h + lane;
-          const bool in = kin && r < a.R;
-          cp_async8(d + k * kXP + 32 * h + lane, a.X + (in ? xr[r] + ko : 0), in);
-        }
+        for (int h = 0; h < kRows / 32; ++h)
+          cp_async8(d + k * kXP + 32 * h + lane, a.X + (ro[h] + ko), kin && rin[h]);
       }
     } else {
-      // lanes: 8 consecutive K entries x 4 rows
+      // lanes: 8 consecutive K entries x 4 rows (two row offsets per lane)
       const int kk = lane & 7, rr = lane >> 3;
-      for (int rb = 4 * warp; rb < kRows; rb += 4 * (kThreads / 32)) {
-        const int r = r0 + rb + rr;
-        const bool rin = r < a.R;
-        const IDX ro = rin ? xr[r] : 0;
-        for (int k0 = 0; k0 < a.KP; k0 += 8) {
-          const int k = k0 + kk;
-          if (k < a.KP) {
-            const bool in = rin && k < a.K;
-            cp_async8(d + k * kXP + rb + rr, a.X + (in ? ro + xk[k] : 0), in);
-          }
+      IDX ro[2];
+      bool rin[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = r0 + 4 * warp + 32 * q + rr;
+        rin[q] = r < a.R;
+        ro[q] = rin[q] ? xr[r] : 0;
+      }
+#pragma unroll 2
+      for (int k0 = 0; k0 < a.KP; k0 += 8) {
+        const int k = k0 + kk;
+        if (k < a.KP) {
+          const IDX ko = xks[k];
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            cp_async8(d + k * kXP + 4 * warp + 32 * q + rr, a.X + (ro[q] + ko), rin[q] && k < a.K);
         }
       }
     }
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
         for (int e = 0; e < 2; ++e) {
           const int n = wc + 8 * j + 2 * t + e;
           if (n >= a.NC) continue;
-          double* q = a.C + (ro + cc[n]);
+          double* q = a.C + (ro + ccs[n]);
           double v = a.alpha * acc[j][2 * h + e];
           if (a.beta != 0.0) v = fma(a.beta, *q, v);
           *q = v;
@@ -180,7 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
 
 template <typename IDX, bool ROWS_UNIT, int NW>
 static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
-  const int smem = (a.KP * (a.NP + 4) + kBufs * a.KP * kXP) * (int)sizeof(double);
+  const int smem = (a.KP * (a.NP + 4) + kBufs * a.KP * kXP) * (int)sizeof(double) +
+                   (a.KP + a.NP) * (int)sizeof(IDX);
   auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW>;
   static int attr = 0;
   if (attr < smem) {
@@ -210,9 +230,10 @@ static int launch_dir(const Args& a, int nsm, cudaStream_t s) {
 }  // namespace skinny
 
 // The skinny path applies to fp64 contractions with K <= 80 and one free extent <= 96 (the
-// small extent becomes the resident operand's columns). Returns 0 when it does not apply,
-// 1 on launch, -1 on a CUDA error.
-int launch_skinny(const LaunchArgs& la, cudaStream_t stream) {
+// small extent becomes the resident operand's columns), by default only when the streamed
+// operand is contiguous along the long bundle. Returns 0 when it does not apply, 1 on launch,
+// -1 on a CUDA error.
+int launch_skinny(const LaunchArgs& la, cudaStream_t stream, bool force) {
   using namespace skinny;
   if (la.f32 || la.K < 1 || la.K > kMaxK) return 0;
   const bool small_n = la.N <= kMaxN;
@@ -231,6 +252,7 @@ int launch_skinny(const LaunchArgs& la, cudaStream_t stream) {
     a.R = la.N; a.NC = la.M;
     rows_unit = !la.b_vec_k;
   }
+  if (!rows_unit && !force) return 0;
   a.C = static_cast<double*>(la.C);
   a.K = la.K;
   a.NP = (a.NC + 15) / 16 * 16;

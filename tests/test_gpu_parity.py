@@ -576,7 +576,7 @@ def test_guard_bands(seed, dtype):
     ("mn-mk-kn", {"m": 4096, "n": 1, "k": 1}, 1.0),        # degenerate N = K = 1
     ("abcde-efbad-cf", {"a": 9, "b": 9, "c": 19, "d": 9, "e": 9, "f": 23}, 0.0),  # fig:bench 0
 ])
-@pytest.mark.parametrize("skinny", ["1", "0"])
+@pytest.mark.parametrize("skinny", ["1", "0", ""])
 def test_skinny_shapes(spec, lens, beta, skinny, monkeypatch):
     monkeypatch.setenv("TC_SKINNY", skinny)   # the library reads it on every call
     lc, la, lb = spec.split("-")
