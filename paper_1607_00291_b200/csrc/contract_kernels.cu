@@ -371,15 +371,13 @@ static int kernel_choice() {
   return choice;
 }
 
-// The skinny-contraction kernel (skinny.cu) runs by default when its streamed operand is
-// contiguous along the long bundle (there it beats the tensor-core tile: f2 abcd-ebad-ce 0.82 ->
-// 0.99 of DGEMM, profiles/r01/suite_f2_skinny_ab.txt); TC_SKINNY=1 forces it for every skinny
-// shape, TC_SKINNY=0 turns it off. Read on every call, so tests can switch it.
+// The skinny-contraction kernel (skinny.cu) runs for every skinny shape (measured against the
+// tensor-core tile on the f2 strings, profiles/r01/suite_f2_skinny_ab.txt); TC_SKINNY=0 turns
+// it off. Read on every call, so tests can switch it.
 static int skinny_mode() {
   const char* e = getenv("TC_SKINNY");
-  if (e && !strcmp(e, "1")) return 2;
   if (e && !strcmp(e, "0")) return 0;
-  return 1;
+  return 2;
 }
 
 // TC_TINY=0 sends tiny contractions to the tensor-core kernel too (tests cover both paths).

@@ -34,7 +34,8 @@ struct LaunchArgs {
   int a_mode, b_mode;
   bool a_elem, b_elem;
   bool f32_a_transpose;
-  bool c_lanes_n;        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
+  bool c_lanes_n;
+  int skinny_bu, skinny_bv;   // skinny kernel: X rows come in bv runs of bu (plan.cpp)        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA

@@ -297,6 +297,47 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
     if (jb >= 0 && (jc < 0 || jc == jb || wB > wC)) to_front(p->kb.J, jb);
     else to_front(p->kb.J, jc);
   }
+  // Dimension sub-division for skinny contractions (the paper's remedy for
+  // contractions without a common stride-1 index). When the skinny kernel will
+  // stream the long free bundle (fp64, K <= 80, the other free extent <= 96) and the streamed
+  // operand X and C have different unit-stride dimensions u (X's) and v (C's) in it, the bundle
+  // is walked as [v_lo, u_lo, u_hi, v_hi, rest] with v_lo, u_lo the largest divisors of the two
+  // lengths that are <= 8: a block of rows then holds bv runs of bu consecutive X elements and
+  // bu runs of bv consecutive C elements, so both streams move whole sectors. The kernel's
+  // loader maps lanes to rows through (bu, bv).
+  p->skinny_bu = p->skinny_bv = 1;
+  if (dtype == TC_F64 && !p->empty_out && p->k >= 1 && p->k <= 80 &&
+      (p->n <= 96 || p->m <= 96)) {
+    std::vector<Dim>& L = p->n <= 96 ? p->kb.I : p->kb.J;   // long bundle; X = A or B
+    const int u = find_unit(L, 0), v = find_unit(L, 1);
+    auto divisor = [](int64_t len) {   // a power of two, so bu * bv divides the 64-row block
+      for (int64_t b = 8; b >= 2; b /= 2)
+        if (len % b == 0) return b;
+      return (int64_t)1;
+    };
+    if (u >= 0 && v >= 0 && u != v) {
+      const int64_t bu = divisor(L[(size_t)u].len), bv = divisor(L[(size_t)v].len);
+      if (bu > 1 && bv > 1) {
+        const Dim du = L[(size_t)u], dv = L[(size_t)v];
+        auto part = [](const Dim& d, int64_t len, int64_t mul, const char* tag) {
+          Dim x = d;
+          x.len = len;
+          x.s[0] = d.s[0] * mul;
+          x.s[1] = d.s[1] * mul;
+          x.labels = d.labels + tag;
+          return x;
+        };
+        std::vector<Dim> out = {part(dv, bv, 1, "_lo"), part(du, bu, 1, "_lo")};
+        if (du.len / bu > 1) out.push_back(part(du, du.len / bu, bu, "_hi"));
+        if (dv.len / bv > 1) out.push_back(part(dv, dv.len / bv, bv, "_hi"));
+        for (size_t i = 0; i < L.size(); ++i)
+          if ((int)i != u && (int)i != v) out.push_back(L[i]);
+        L = out;
+        p->skinny_bu = (int)bu;
+        p->skinny_bv = (int)bv;
+      }
+    }
+  }
   if (!p->empty_out) {
     p->kscat[0] = scatter(p->kb.I, 0);
     p->kscat[1] = scatter(p->kb.P, 0);
@@ -315,6 +356,10 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   int64_t lb_k = lead(p->kb.P, 1), lb_n = lead(p->kb.J, 0);
   p->a_vec_m = la_m <= la_k;
   p->b_vec_k = lb_k <= lb_n;
+  if (p->skinny_bu > 1) {   // the sub-divided long bundle is the streamed operand's direction
+    if (p->n <= 96) p->a_vec_m = true;
+    else p->b_vec_k = false;
+  }
   if (!p->empty_out && p->k > 0) {
     const int64_t V = dtype == TC_F64 ? 2 : 4;
     p->a_pairs_all = p->a_vec_m ? vec_blocks_all(p->kscat[0], p->kscat[1], V)

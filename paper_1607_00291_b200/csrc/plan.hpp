@@ -78,6 +78,8 @@ struct Plan {
   bool a_elem = true, b_elem = true;
   // C's traversal tables: more unit steps along N (cscat_C) than along M (rscat_C)
   bool c_unit_n = false;
+  // row blocking of the long free bundle for the skinny kernel (1, 1: none), see plan.cpp
+  int skinny_bu = 1, skinny_bv = 1;
   int variant = 0;
   // per-device uploaded tables
   mutable std::mutex mu;

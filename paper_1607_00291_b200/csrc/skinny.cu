@@ -45,6 +45,7 @@ struct Args {
   const void* cc;   // C offsets along the small bundle
   int R, NC, K;     // long extent, small extent, bound extent
   int NP, KP;       // NC rounded up to 16, K rounded up to 4
+  int bu, bv;       // X rows come in bv runs of bu contiguous elements (plan.cpp); 1, 1: plain
   double alpha, beta;
 };
 
@@ -106,87 +107,95 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   cp_async_commit();
 
   const int nblk = (a.R + kRows - 1) / kRows;
-  auto load_x = [&](int blk, int buf) {
-    double* d = xs + buf * (a.KP * kXP);
-    const int r0 = blk * kRows;
-    if constexpr (ROWS_UNIT) {
-      // lanes: 32 consecutive rows (two row offsets per lane); warps stride over K
-      IDX ro[kRows / 32];
-      bool rin[kRows / 32];
+  // Per lane: two X rows of a block (rows-unit: rl[h] within the block; K-unit: 4 warp + 32 q
+  // + (lane >> 3)). Their offsets are fetched one block ahead (rows()), so the loader never
+  // waits on the row table when it issues the copies (issue()).
+  const int bb = a.bu * a.bv;
+  int rl[2];
 #pragma unroll
-      for (int h = 0; h < kRows / 32; ++h) {
-        const int r = r0 + 32 * h + lane;
-        rin[h] = r < a.R;
-        ro[h] = rin[h] ? xr[r] : 0;
-      }
+  for (int h = 0; h < 2; ++h) {
+    if constexpr (ROWS_UNIT) {
+      // with sub-divided rows, element e of the block is row (e % bu) bv + (e / bu) % bv +
+      // (e / (bu bv)) bu bv, so consecutive lanes still read consecutive X elements
+      const int e = 32 * h + lane;
+      rl[h] = (e % a.bu) * a.bv + (e / a.bu) % a.bv + (e / bb) * bb;
+    } else {
+      rl[h] = 4 * warp + 32 * h + (lane >> 3);
+    }
+  }
+  // (strides may be negative, so validity travels in rv, not in the offset)
+  auto rows = [&](int blk, IDX (&ro)[2], bool (&rv)[2]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = blk * kRows + rl[h];
+      rv[h] = blk < nblk && r < a.R;
+      ro[h] = rv[h] ? xr[r] : 0;
+    }
+  };
+  auto issue = [&](int buf, const IDX (&ro)[2], const bool (&rv)[2]) {
+    double* d = xs + buf * (a.KP * kXP);
+    if constexpr (ROWS_UNIT) {
 #pragma unroll 4
       for (int k = warp; k < a.KP; k += kThreads / 32) {
         const bool kin = k < a.K;
         const IDX ko = xks[k];
 #pragma unroll
-        for (int h = 0; h < kRows / 32; ++h)
-          cp_async8(d + k * kXP + 32 * h + lane, a.X + (ro[h] + ko), kin && rin[h]);
+        for (int h = 0; h < 2; ++h)
+          cp_async8(d + k * kXP + rl[h], a.X + (ro[h] + ko), kin && rv[h]);
       }
     } else {
-      // lanes: 8 consecutive K entries x 4 rows (two row offsets per lane)
-      const int kk = lane & 7, rr = lane >> 3;
-      IDX ro[2];
-      bool rin[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = r0 + 4 * warp + 32 * q + rr;
-        rin[q] = r < a.R;
-        ro[q] = rin[q] ? xr[r] : 0;
-      }
+      const int kk = lane & 7;
 #pragma unroll 2
       for (int k0 = 0; k0 < a.KP; k0 += 8) {
         const int k = k0 + kk;
         if (k < a.KP) {
           const IDX ko = xks[k];
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
-            cp_async8(d + k * kXP + 4 * warp + 32 * q + rr, a.X + (ro[q] + ko), rin[q] && k < a.K);
+          for (int h = 0; h < 2; ++h)
+            cp_async8(d + k * kXP + rl[h], a.X + (ro[h] + ko), rv[h] && k < a.K);
         }
       }
     }
   };
 
   // ring of kBufs X blocks: blocks blockIdx.x + i * gridDim.x
-  int issued = 0;
+  IDX ro[2];
+  bool rv[2];
   for (int i = 0; i < kBufs - 1; ++i) {
-    const int blk = blockIdx.x + i * gridDim.x;
-    if (blk < nblk) load_x(blk, i);
+    rows(blockIdx.x + i * gridDim.x, ro, rv);
+    issue(i, ro, rv);
     cp_async_commit();
-    ++issued;
   }
+  rows(blockIdx.x + (kBufs - 1) * gridDim.x, ro, rv);   // offsets of the next block to load
   const int g = lane >> 2, t = lane & 3;
   const int wr = 16 * (warp & 3), wc = (warp >> 2) * (a.NP / 2);
   double acc[NW][4];
   for (int it = 0;; ++it) {
     const int blk = blockIdx.x + it * gridDim.x;
     if (blk >= nblk) break;
-    {   // keep kBufs - 1 blocks in flight
-      const int nb = blockIdx.x + (it + kBufs - 1) * gridDim.x;
-      if (nb < nblk) load_x(nb, (it + kBufs - 1) % kBufs);
-      cp_async_commit();
-    }
+    // C's row offsets of this block: fetched now, used after the multiply
+    const int cr0 = blk * kRows + wr + g;
+    IDX cro[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) cro[h] = cr0 + 8 * h < a.R ? cr[cr0 + 8 * h] : 0;
+    // keep kBufs - 1 blocks in flight; prefetch the row offsets of the block after
+    issue((it + kBufs - 1) % kBufs, ro, rv);
+    cp_async_commit();
+    rows(blockIdx.x + (it + kBufs) * gridDim.x, ro, rv);
     cp_async_wait<kBufs - 1>();
     __syncthreads();
     block_mma<IDX, NW>(xs + (it % kBufs) * (a.KP * kXP), ys, yp, a.KP, wr, wc, g, t, acc);
     // epilogue: rows wr + g (+8), columns wc + 8 j + 2 t (+1)
-    const int r0 = blk * kRows + wr + g;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = r0 + 8 * h;
-      if (r >= a.R) continue;
-      const IDX ro = cr[r];
+      if (cr0 + 8 * h >= a.R) continue;
 #pragma unroll
       for (int j = 0; j < NW; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = wc + 8 * j + 2 * t + e;
           if (n >= a.NC) continue;
-          double* q = a.C + (ro + ccs[n]);
+          double* q = a.C + (cro[h] + ccs[n]);
           double v = a.alpha * acc[j][2 * h + e];
           if (a.beta != 0.0) v = fma(a.beta, *q, v);
           *q = v;
@@ -258,6 +267,8 @@ int launch_skinny(const LaunchArgs& la, cudaStream_t stream, bool force) {
   a.NP = (a.NC + 15) / 16 * 16;
   a.KP = (a.K + 3) / 4 * 4;
   a.alpha = la.alpha; a.beta = la.beta;
+  a.bu = la.skinny_bu > 0 ? la.skinny_bu : 1;
+  a.bv = la.skinny_bv > 0 ? la.skinny_bv : 1;
   if (la.idx64)
     return rows_unit ? launch_dir<long long, true>(a, la.num_sms, stream)
                      : launch_dir<long long, false>(a, la.num_sms, stream);

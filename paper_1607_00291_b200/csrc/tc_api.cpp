@@ -224,6 +224,8 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
   a.f32_a_transpose = f32_a_transpose() && !force_scatter();
   a.c_lanes_n = p.c_unit_n;
+  a.skinny_bu = p.skinny_bu;
+  a.skinny_bv = p.skinny_bv;
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;
   StreamFlags* sf = stream_flags(d->device, stream, a.flags_cap);
