@@ -290,8 +290,44 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
     if (ia >= 0 && (ic < 0 || ic == ia || wA > wC)) { to_front(p->kb.I, ia); a_m = true; }
     else to_front(p->kb.I, ic);
   }
-  bool a_k = !a_m && unit_front(p->kb.P, 0);
-  bool b_k = a_k ? (!p->kb.P.empty() && p->kb.P[0].s[1] == 1) : unit_front(p->kb.P, 1);
+  // Dimension sub-division of P: when A and B both read along
+  // K but have different unit-stride dimensions u (A's) and w (B's) there, the bundle is walked
+  // as [u_lo, w_lo, u_hi, w_hi, rest] with u_lo, w_lo of length <= 4 (powers of two dividing
+  // the lengths), so within each K step both operands read runs of consecutive elements
+  // instead of one of them gathering element by element.
+  p->k_blocked = false;
+  if (!a_m && p->k > 0) {
+    const int u = find_unit(p->kb.P, 0), w = find_unit(p->kb.P, 1);
+    auto divisor = [](int64_t len) {
+      for (int64_t b = 4; b >= 2; b /= 2)
+        if (len % b == 0) return b;
+      return (int64_t)1;
+    };
+    if (u >= 0 && w >= 0 && u != w) {
+      const Dim du = p->kb.P[(size_t)u], dw = p->kb.P[(size_t)w];
+      const int64_t bu = divisor(du.len), bw = divisor(dw.len);
+      if (bu > 1 && bw > 1) {
+        auto part = [](const Dim& d, int64_t len, int64_t mul, const char* tag) {
+          Dim x = d;
+          x.len = len;
+          x.s[0] = d.s[0] * mul;
+          x.s[1] = d.s[1] * mul;
+          x.labels = d.labels + tag;
+          return x;
+        };
+        std::vector<Dim> out = {part(du, bu, 1, "_lo"), part(dw, bw, 1, "_lo")};
+        if (du.len / bu > 1) out.push_back(part(du, du.len / bu, bu, "_hi"));
+        if (dw.len / bw > 1) out.push_back(part(dw, dw.len / bw, bw, "_hi"));
+        for (size_t i = 0; i < p->kb.P.size(); ++i)
+          if ((int)i != u && (int)i != w) out.push_back(p->kb.P[i]);
+        p->kb.P = out;
+        p->k_blocked = true;
+      }
+    }
+  }
+  bool a_k = !a_m && (p->k_blocked || unit_front(p->kb.P, 0));
+  bool b_k = p->k_blocked ||
+             (a_k ? (!p->kb.P.empty() && p->kb.P[0].s[1] == 1) : unit_front(p->kb.P, 1));
   if (!b_k) {
     const int jb = find_unit(p->kb.J, 0), jc = find_unit(p->kb.J, 1);
     if (jb >= 0 && (jc < 0 || jc == jb || wB > wC)) to_front(p->kb.J, jb);
@@ -356,6 +392,10 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   int64_t lb_k = lead(p->kb.P, 1), lb_n = lead(p->kb.J, 0);
   p->a_vec_m = la_m <= la_k;
   p->b_vec_k = lb_k <= lb_n;
+  if (p->k_blocked) {   // both operands read their runs along the sub-divided K
+    p->a_vec_m = false;
+    p->b_vec_k = true;
+  }
   if (p->skinny_bu > 1) {   // the sub-divided long bundle is the streamed operand's direction
     if (p->n <= 96) p->a_vec_m = true;
     else p->b_vec_k = false;

@@ -80,6 +80,7 @@ struct Plan {
   bool c_unit_n = false;
   // row blocking of the long free bundle for the skinny kernel (1, 1: none), see plan.cpp
   int skinny_bu = 1, skinny_bv = 1;
+  bool k_blocked = false;   // P walked as [u_lo, w_lo, u_hi, w_hi, ...] (plan.cpp)
   int variant = 0;
   // per-device uploaded tables
   mutable std::mutex mu;
