@@ -159,8 +159,11 @@ def test_planner_rankk_structures(i):
 def test_traversal_tables_reproduce_contraction(seed):
     """The kernel's traversal-order tables (reading R16) are a relinearisation of the same
     contraction: gathering through them and multiplying gives the brute-force result."""
+    _check_traversal(W.random_tiny_case(seed, max_len=5, dist="int"))
+
+
+def _check_traversal(case):
     import oracle
-    case = W.random_tiny_case(seed, max_len=5, dist="int")
     A, B, C = W.make_tensors(case)
     (la, sa, ta), (lb, sb, tb), (lc, sc, tcs) = _shapes(case)
     p = tc.Plan(case.spec, case.dtype, (sa, sb, sc), (ta, tb, tcs))
@@ -182,3 +185,28 @@ def test_traversal_tables_reproduce_contraction(seed):
     # and it is the paper-order table set up to a permutation of rows/columns
     for i in range(6):
         assert sorted(p.traversal_scatter(i)) == sorted(p.scatter(i))
+    return p
+
+
+def test_dimension_subdivision_of_the_long_bundle():
+    """f4: fig:bench's abcde-efbad-cf shape class at lengths 4 -- A's unit-stride
+    index e and C's a are both in I; the traversal interleaves a 4 x 4 block of them, so the
+    first rows step C by 1 and A by its a-stride, and row 4 is A's next element."""
+    lens = {x: 4 for x in "abcdef"}
+    case = W.Case("sub_I", "abcde", "efbad", "cf", lens, dist="int", alpha=2.0, beta=0.0,
+                  c_init="zero", seed=3)
+    p = _check_traversal(case)
+    rA, rC = p.traversal_scatter(0), p.traversal_scatter(4)
+    assert rC[:4] == [0, 1, 2, 3]
+    assert rA[:4] == [0, 64, 128, 192] and rA[4] == 1
+
+
+def test_dimension_subdivision_of_the_bound_bundle():
+    """f4 for P: A's unit-stride bound index k and B's d differ (cfg4 case 5's class,
+    roc-krdo-dck); the K traversal takes 4 k then 4 d, so A reads runs of 4 and so does B."""
+    lens = {"r": 6, "o": 5, "k": 8, "d": 4, "c": 7}
+    case = W.Case("sub_P", "roc", "krdo", "dck", lens, dist="int", alpha=1.0, beta=0.5,
+                  c_init="dist", seed=4)
+    p = _check_traversal(case)
+    cA, rB = p.traversal_scatter(1), p.traversal_scatter(2)
+    assert cA[:4] == [0, 1, 2, 3] and rB[4:8] == [1, 1 + 4 * 7, 1 + 2 * 4 * 7, 1 + 3 * 4 * 7]

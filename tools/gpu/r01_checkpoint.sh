@@ -16,4 +16,5 @@ CMDS="python bench.py --small --steps 1 --warmup 1 --no-e2e --no-cpu --no-gemm"
 timeout 600 $CMDS > gpurun_out/plain_small.log 2>&1 && \
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tc_ -s 1 -c 1 -o gpurun_out/prof_small $CMDS > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> gpurun_out/ncu_full.log
-tail -2 gpurun_out/build.log; tail -3 gpurun_out/smoke.log; tail -15 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.log; tail -5 gpurun_out/bench.err; tail -3 gpurun_out/ncu_launch.log gpurun_out/ncu_traffic.log gpurun_out/ncu_full.log
+tail -2 gpurun_out/build.log; tail -3 gpurun_out/smoke.log; tail -15 gpurun_out/pytest_gpu.log; cat gpurun_out/bench.log; tail -5 gpurun_out/bench.err; for f in gpurun_out/ncu_launch.log gpurun_out/ncu_traffic.log gpurun_out/ncu_full.log; do tail -n 3 $f; done
+python tools/ncu_summary.py gpurun_out/prof_small.ncu-rep > gpurun_out/summary_small.txt 2>&1; ncu -i gpurun_out/prof_small.ncu-rep --page source --csv > gpurun_out/source_small.csv 2>/dev/null; rm -f gpurun_out/prof_small.ncu-rep
