@@ -54,6 +54,15 @@ template <typename T> constexpr int stages() {
 // floats, row pitch kEpiLD (a multiple of 4 for 16-byte accesses)
 constexpr int kEpiLD = 64 + 4;
 constexpr int kEpiWarpFloats = 32 * kEpiLD;
+// DMMA epilogue staging (fp64, when C's unit stride runs along M): per consumer warp 16 rows
+// x 32 columns of its block at a time, [n][m] doubles with pitch kEpiDLD; four passes. Off by
+// default: measured slower than the direct fragment stores (which already fill whole sectors)
+// on the small-K families (f1 k16: 0.85 -> 0.72 of DGEMM; profiles/r01/ab_dmma_staged.txt).
+#ifndef TC_DMMA_STAGED
+#define TC_DMMA_STAGED 0
+#endif
+constexpr int kEpiDLD = 16 + 4;
+constexpr int kEpiWarpDoubles = 32 * kEpiDLD;
 constexpr int kSmemLimit = 232448;   // 227 KB of dynamic shared memory per CTA
 // Tile rasterisation group height. With K in the tens of thousands a CTA's A and B panels are
 // tens of MB, and the CTAs of a wave drift apart in K faster than L2 (126 MB, turned over every
@@ -644,7 +653,8 @@ template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA>
 constexpr int smem_bytes(int stages_) {
   return ((stages_ * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) * (int)sizeof(T) + 15) / 16) * 16 +
          2 * stages_ * (int)sizeof(uint64_t) + NCW * kWarpTab * (int)sizeof(IDX) +
-         (FFMA ? NCW * kEpiWarpFloats * (int)sizeof(float) : 0);
+         (FFMA ? NCW * kEpiWarpFloats * (int)sizeof(float)
+               : (TC_DMMA_STAGED ? NCW * kEpiWarpDoubles * (int)sizeof(double) : 0));
 }
 template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA>
 constexpr int ring_stages() {
@@ -675,6 +685,8 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
   IDX* wtab = reinterpret_cast<IDX*>(empty + STAGES) + (threadIdx.x >> 5) * kWarpTab;
   float* epi = reinterpret_cast<float*>(reinterpret_cast<IDX*>(empty + STAGES) + NCW * kWarpTab) +
                (threadIdx.x >> 5) * kEpiWarpFloats;
+  double* epid = reinterpret_cast<double*>(reinterpret_cast<IDX*>(empty + STAGES) + NCW * kWarpTab) +
+                 (threadIdx.x >> 5) * kEpiWarpDoubles;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -871,6 +883,52 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
             if (accumulate) v += old[i];
             else if (beta != 0.0) v = fma(beta, (double)old[i], v);
             if (nin && min_[i]) C[rc[i] + cc] = static_cast<T>(v);
+          }
+        }
+      }
+    } else if (TC_DMMA_STAGED && !c_lanes_n) {
+      // DMMA epilogue through shared memory, 16 rows at a time: lanes 0-15 and 16-31 write 16
+      // consecutive rows of two columns, i.e. two 128-byte runs per warp store when C is
+      // unit-stride along M (the fragment layout gives four 64-byte pieces).
+      cp_async_wait_all();
+      const bool read_c = accumulate || beta != 0.0;
+      const int ri = lane & 15, cp = lane >> 4;
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass) {
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            epid[(mk.col(c) - mk.wn) * kEpiDLD + (mk.row(2 * pass + h) - mk.wm - 16 * pass)] =
+                static_cast<double>(mk.value(2 * pass + h, c));
+        __syncwarp();
+        const int mrow = 16 * pass + ri;            // row within the warp block
+        const bool min_ = m0 + mk.wm + mrow < M;
+        const IDX rc = wtab[mrow];
+#pragma unroll 2
+        for (int j0 = 0; j0 < 16; j0 += 8) {
+          double old[8];
+          IDX cc[8];
+          bool ok[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int col = 2 * (j0 + j) + cp;
+            cc[j] = wtab[WM + col];
+            ok[j] = min_ && n0 + mk.wn + col < N;
+            old[j] = 0.0;
+            if (read_c && ok[j]) {
+              const T* q = C + (rc + cc[j]);
+              old[j] = static_cast<double>(accumulate ? __ldcg(q) : *q);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int col = 2 * (j0 + j) + cp;
+            double v = alpha * epid[col * kEpiDLD + ri];
+            if (accumulate) v += old[j];
+            else if (beta != 0.0) v = fma(beta, old[j], v);
+            if (ok[j]) C[rc + cc[j]] = static_cast<T>(v);
           }
         }
       }
