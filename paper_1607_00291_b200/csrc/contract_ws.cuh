@@ -1044,7 +1044,9 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   }
   int* flags = a.flags;
   const int grid = sc.D > 0 ? sc.P : sc.P_sk;
-  sc.wave_sync = a.wave_sync && a.wave_base != nullptr && sc.D >= 2 * sc.P;
+  // wave alignment only pays when a tile's K panels are long enough for L2 sharing to matter;
+  // with short K loops the per-wave wait is pure overhead (f1 k5: 15% of samples at the barrier)
+  sc.wave_sync = a.wave_sync && a.wave_base != nullptr && sc.D >= 2 * sc.P && KT >= 64;
   if (sc.wave_sync) {
     sc.wave_base = *a.wave_base;
     *a.wave_base += (unsigned)sc.D;   // every whole tile adds one to the counter
