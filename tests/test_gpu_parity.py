@@ -586,3 +586,43 @@ def test_skinny_shapes(spec, lens, beta, skinny, monkeypatch):
     case.dist, case.alpha = "int", 2.0
     case.beta = 0.5 if beta else 0.0
     check(case, bitwise=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# negative strides (accepted for A, B and C by the C ABI, reading R7) through the raw binding
+# ---------------------------------------------------------------------------------------------
+
+def _reversed_desc(t_dev, labels, flip):
+    """Descriptor of the device tensor t_dev walked backwards along the dims in `flip`: the
+    data pointer moves to the last element of each flipped dim and its stride changes sign."""
+    lens, strides = list(t_dev.shape), list(t_dev.stride())
+    off = 0
+    for d in flip:
+        off += (lens[d] - 1) * strides[d]
+        strides[d] = -strides[d]
+    ptr = t_dev.data_ptr() + off * t_dev.element_size()
+    return tc().Desc(labels, lens, strides, ptr)
+
+
+@pytest.mark.usefixtures("both_small_paths")
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("lens", [{"m": 300, "n": 200, "k": 150},    # tensor-core tile kernel
+                                  {"m": 5000, "n": 40, "k": 30},     # skinny kernel (fp64)
+                                  {"m": 33, "n": 17, "k": 9}])       # tiny kernel
+def test_negative_strides(lens, dtype):
+    g = torch.Generator().manual_seed(7)
+    m, n, k = lens["m"], lens["n"], lens["k"]
+    A = torch.randint(-4, 5, (m, k), generator=g).to(dtype)
+    B = torch.randint(-4, 5, (k, n), generator=g).to(dtype)
+    C = torch.randint(-4, 5, (m, n), generator=g).to(dtype)
+    # reference: A read backwards along m, B backwards along k, C written backwards along n
+    Ar, Br = A.flip(0), B.flip(0)
+    ref = C.flip(1).clone()
+    oracle.contract("mn-mk-kn", Ar, Br, ref, 2.0, 0.5)
+    Ad, Bd, Cd = A.cuda(), B.cuda(), C.cuda()
+    code = tc()._dtype_code(dtype)
+    tc().tc_contract(code, 2.0, _reversed_desc(Ad, "mk", [0]), _reversed_desc(Bd, "kn", [0]), 0.5,
+                     _reversed_desc(Cd, "mn", [1]), None)
+    torch.cuda.synchronize()
+    assert torch.equal(Cd.cpu().flip(1), ref)
+
