@@ -170,14 +170,21 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   const int g = lane >> 2, t = lane & 3;
   const int wr = 16 * (warp & 3), wc = (warp >> 2) * (a.NP / 2);
   double acc[NW][4];
+  // C's row offsets of a block are fetched one block ahead as well
+  auto crows = [&](int blk, IDX (&o)[2]) {
+    const int r0 = blk * kRows + wr + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) o[h] = (blk < nblk && r0 + 8 * h < a.R) ? cr[r0 + 8 * h] : 0;
+  };
+  IDX cro[2], cro_next[2];
+  crows(blockIdx.x, cro_next);
   for (int it = 0;; ++it) {
     const int blk = blockIdx.x + it * gridDim.x;
     if (blk >= nblk) break;
-    // C's row offsets of this block: fetched now, used after the multiply
     const int cr0 = blk * kRows + wr + g;
-    IDX cro[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) cro[h] = cr0 + 8 * h < a.R ? cr[cr0 + 8 * h] : 0;
+    for (int h = 0; h < 2; ++h) cro[h] = cro_next[h];
+    crows(blk + gridDim.x, cro_next);
     // keep kBufs - 1 blocks in flight; prefetch the row offsets of the block after
     issue((it + kBufs - 1) % kBufs, ro, rv);
     cp_async_commit();
