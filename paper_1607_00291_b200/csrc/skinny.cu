@@ -30,7 +30,7 @@ constexpr int kRows = 64;           // X rows per block
 constexpr int kThreads = 256;
 constexpr int kMaxN = 96;           // small free extent (padded to a multiple of 16)
 constexpr int kMaxK = 80;           // bound extent (padded to a multiple of 4)
-constexpr int kBufs = 3;            // X ring depth
+constexpr int kBufsMax = 6;         // X ring depth: 6 when it fits in shared memory, else 3
 constexpr int kXP = kRows + 4;      // [k][row] pitch (doubles): conflict-free fragment loads
 
 struct Args {
@@ -77,7 +77,7 @@ __device__ __forceinline__ void block_mma(const double* xs, const double* ys, in
 
 // ROWS_UNIT: X is contiguous along its rows (lanes take consecutive rows); otherwise along K
 // (lanes take 8 consecutive K entries of 4 rows).
-template <typename IDX, bool ROWS_UNIT, int NW>
+template <typename IDX, bool ROWS_UNIT, int NW, int kBufs>
 __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int yp = a.NP + 4;   // [k][col] pitch of Y (doubles), = 8 (mod 16) words per row
@@ -213,11 +213,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   cp_async_wait_all();
 }
 
-template <typename IDX, bool ROWS_UNIT, int NW>
-static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
-  const int smem = (a.KP * (a.NP + 4) + kBufs * a.KP * kXP) * (int)sizeof(double) +
+template <typename IDX, bool ROWS_UNIT, int NW, int NBUF>
+static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
+  const int smem = (a.KP * (a.NP + 4) + NBUF * a.KP * kXP) * (int)sizeof(double) +
                    (a.KP + a.NP) * (int)sizeof(IDX);
-  auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW>;
+  auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW, NBUF>;
   static int attr = 0;
   if (attr < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
@@ -229,6 +229,16 @@ static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
   const int grid = nblk < nsm ? nblk : nsm;
   kern<<<grid, kThreads, smem, s>>>(a);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// Ring depth: 3. A 6-deep ring (more bytes in flight per SM) measured slower on the HBM-bound
+// f2 strings, so launch_nb<..., kBufsMax> is kept only as the switch for that experiment.
+template <typename IDX, bool ROWS_UNIT, int NW>
+static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
+  const int deep = (a.KP * (a.NP + 4) + kBufsMax * a.KP * kXP) * (int)sizeof(double) +
+                   (a.KP + a.NP) * (int)sizeof(IDX);
+  (void)deep;   // measured: 6 buffers made the HBM-bound f2 strings slower (0.84 -> 0.64 of DGEMM)
+  return launch_nb<IDX, ROWS_UNIT, NW, 3>(a, nsm, s);
 }
 
 template <typename IDX, bool ROWS_UNIT>
