@@ -30,7 +30,7 @@ constexpr int kRows = 64;           // X rows per block
 constexpr int kThreads = 256;
 constexpr int kMaxN = 96;           // small free extent (padded to a multiple of 16)
 constexpr int kMaxK = 80;           // bound extent (padded to a multiple of 4)
-constexpr int kBufsMax = 6;         // X ring depth: 6 when it fits in shared memory, else 3
+constexpr int kBufs = 3;            // X ring depth
 constexpr int kXP = kRows + 4;      // [k][row] pitch (doubles): conflict-free fragment loads
 
 struct Args {
@@ -231,14 +231,11 @@ static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-// Ring depth: 3. A 6-deep ring (more bytes in flight per SM) measured slower on the HBM-bound
-// f2 strings, so launch_nb<..., kBufsMax> is kept only as the switch for that experiment.
+// Ring depth 3 (kBufs). A 6-deep ring, for more bytes in flight per SM, measured slower on
+// the HBM-bound f2 strings (0.84 -> 0.64 of DGEMM).
 template <typename IDX, bool ROWS_UNIT, int NW>
 static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
-  const int deep = (a.KP * (a.NP + 4) + kBufsMax * a.KP * kXP) * (int)sizeof(double) +
-                   (a.KP + a.NP) * (int)sizeof(IDX);
-  (void)deep;   // measured: 6 buffers made the HBM-bound f2 strings slower (0.84 -> 0.64 of DGEMM)
-  return launch_nb<IDX, ROWS_UNIT, NW, 3>(a, nsm, s);
+  return launch_nb<IDX, ROWS_UNIT, NW, kBufs>(a, nsm, s);
 }
 
 template <typename IDX, bool ROWS_UNIT>
