@@ -626,3 +626,28 @@ def test_negative_strides(lens, dtype):
     torch.cuda.synchronize()
     assert torch.equal(Cd.cpu().flip(1), ref)
 
+
+
+# ---------------------------------------------------------------------------------------------
+# multi-GPU sharding on one device: every rank's shard contraction (zero-copy narrowed views,
+# dist.contract_shard, the call bench.py makes per GPU) assembled = the full contraction
+# ---------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_blocks_assemble_full_result(world):
+    from paper_1607_00291_b200 import dist as tdist
+    case = W.cfg5(12, 6)
+    case.dist = "int"
+    Ad, Bd, _ = W.make_tensors(case, "cuda", gen_device="cpu")
+    full = W.colmajor_view(torch.full((math.prod(case.shape(case.lab_c)),), float("nan"),
+                                      dtype=torch.float64, device="cuda"), case.shape(case.lab_c))
+    tc().contract(case.spec, Ad, Bd, full, 1.0, 0.0)
+    assembled = torch.full_like(full, float("nan"))
+    for rank in range(world):
+        ranges = tdist.shard_ranges(world, rank, case.lens, "abc")
+        shape = tdist.shard_shape(case.lab_c, case.lens, ranges)
+        Cs = W.colmajor_view(torch.empty(math.prod(shape), dtype=torch.float64, device="cuda"), shape)
+        tdist.contract_shard(case.spec, Ad, Bd, Cs, ranges, 1.0, 0.0)
+        tdist.narrow(assembled, case.lab_c, ranges).copy_(Cs)
+    torch.cuda.synchronize()
+    assert torch.equal(assembled, full)
