@@ -647,6 +647,19 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }
+// Stores of C. TC_C_STREAM_STORE=1 sends final values with the streaming hint (st.global.cs,
+// evict-first; a stream-K piece that a later piece reads back is stored normally). Off: it
+// measured slower, most on the C-write-bound shapes (f1 k16 0.88 -> 0.70, f2 K=18 strings
+// 0.84-0.90 -> 0.70-0.73 of DGEMM; profiles/r01/ab_stream_store.txt).
+#ifndef TC_C_STREAM_STORE
+#define TC_C_STREAM_STORE 0
+#endif
+template <typename T>
+__device__ __forceinline__ void store_c(T* p, T v, bool keep) {
+  if (TC_C_STREAM_STORE && !keep) __stcs(p, v);
+  else *p = v;
+}
+
 __device__ __forceinline__ void producers_sync() {
   asm volatile("bar.sync 2, %0;\n" ::"n"(NPT) : "memory");
 }
@@ -827,6 +840,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       }
     }
     const bool accumulate = split && piece > 0;
+    const bool keep_c = split && ke < sched.KT;   // a later piece reads this tile back
 
     if constexpr (FFMA) {
       // FFMA epilogue through shared memory: the FFMA micro-kernel's thread layout puts a
@@ -882,8 +896,8 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
             double vb = alpha * static_cast<double>(src[lane + 32]);
             if (accumulate) { va += olda[j]; vb += oldb[j]; }
             else if (beta != 0.0) { va = fma(beta, (double)olda[j], va); vb = fma(beta, (double)oldb[j], vb); }
-            if (ina && nin[j]) C[rca + cc[j]] = static_cast<T>(va);
-            if (inb && nin[j]) C[rcb + cc[j]] = static_cast<T>(vb);
+            if (ina && nin[j]) store_c(C + (rca + cc[j]), static_cast<T>(va), keep_c);
+            if (inb && nin[j]) store_c(C + (rcb + cc[j]), static_cast<T>(vb), keep_c);
           }
         }
       } else {
@@ -910,7 +924,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
             double v = alpha * static_cast<double>(xv[i]);
             if (accumulate) v += old[i];
             else if (beta != 0.0) v = fma(beta, (double)old[i], v);
-            if (nin && min_[i]) C[rc[i] + cc] = static_cast<T>(v);
+            if (nin && min_[i]) store_c(C + (rc[i] + cc), static_cast<T>(v), keep_c);
           }
         }
       }
@@ -956,7 +970,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
             double v = alpha * epid[col * kEpiDLD + ri];
             if (accumulate) v += old[j];
             else if (beta != 0.0) v = fma(beta, old[j], v);
-            if (ok[j]) C[rc + cc[j]] = static_cast<T>(v);
+            if (ok[j]) store_c(C + (rc + cc[j]), static_cast<T>(v), keep_c);
           }
         }
       }
@@ -1006,7 +1020,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
           double v = alpha * static_cast<double>(mk.value(2 * r2 + h, c));
           if (accumulate) v += old[h][c];
           else if (beta != 0.0) v = fma(beta, old[h][c], v);
-          C[rc[h] + cc[c]] = static_cast<T>(v);
+          store_c(C + (rc[h] + cc[c]), static_cast<T>(v), keep_c);
         }
       }
     }
