@@ -682,3 +682,19 @@ def test_int64_offsets_large_span(lens):
     assert torch.equal(Cd.cpu(), ref)
     del big
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("alpha,beta", [(1.5, 0.0), (0.0, 0.5), (-1.0, 2.0)])
+def test_host_path_dtypes_and_scalars(dtype, alpha, beta):
+    """tc_contract_host on both element types; alpha = 0 uploads only C (R1)."""
+    case = W.cfg3(True, v=48, o=24)       # 48 MB operands: chunked along C's outer label
+    case.dtype, case.dist, case.alpha, case.beta, case.c_init = dtype, "int", alpha, beta, "dist"
+    A, B, C = W.make_tensors(case, "cpu")
+    if alpha == 0.0:
+        A.fill_(float("nan")); B.fill_(float("nan"))
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, alpha, beta)
+    Cp = C.clone().pin_memory()
+    tc().contract_host(case.spec, A.pin_memory(), B.pin_memory(), Cp, alpha, beta)
+    assert torch.equal(Cp, ref)
