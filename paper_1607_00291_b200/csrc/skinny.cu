@@ -253,9 +253,10 @@ static int launch_dir(const Args& a, int nsm, cudaStream_t s) {
 }  // namespace skinny
 
 // The skinny path applies to fp64 contractions with K <= 80 and one free extent <= 96 (the
-// small extent becomes the resident operand's columns), by default only when the streamed
-// operand is contiguous along the long bundle. Returns 0 when it does not apply, 1 on launch,
-// -1 on a CUDA error.
+// small extent becomes the resident operand's columns). `force` = false restricts it to a
+// streamed operand that is contiguous along the long bundle (launch_contract passes true unless
+// TC_SKINNY=0 turns the path off). Returns 0 when it does not apply, 1 on launch, -1 on a CUDA
+// error.
 int launch_skinny(const LaunchArgs& la, cudaStream_t stream, bool force) {
   using namespace skinny;
   if (la.f32 || la.K < 1 || la.K > kMaxK) return 0;
