@@ -989,6 +989,19 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       cc[c] = wtab[WM + mk.col(c) - mk.wn];
     }
     const bool read_c = accumulate || beta != 0.0;
+    if (!read_c && m0 + BM <= M && n0 + BN <= N) {
+      // interior tile, C write-only: no bounds checks, no reads, all offsets up front (the
+      // common case of small-K contractions, where the epilogue is most of the work)
+      IDX rc[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) rc[r] = wtab[mk.row(r) - mk.wm];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          store_c(C + (rc[r] + cc[c]), static_cast<T>(alpha * static_cast<double>(mk.value(r, c))),
+                  keep_c);
+    } else
 #pragma unroll
     for (int r2 = 0; r2 < 4; ++r2) {
       int mm[2];
