@@ -192,21 +192,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
     cp_async_wait<kBufs - 1>();
     __syncthreads();
     block_mma<IDX, NW>(xs + (it % kBufs) * (a.KP * kXP), ys, yp, a.KP, wr, wc, g, t, acc);
-    // epilogue: rows wr + g (+8), columns wc + 8 j + 2 t (+1)
+    // epilogue: rows wr + g (+8), columns wc + 8 j + 2 t (+1). A full block with every column
+    // in range and beta == 0 stores without checks (the streaming case this kernel is for).
+    if (a.beta == 0.0 && cr0 + 8 < a.R && a.NC == a.NP) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (cr0 + 8 * h >= a.R) continue;
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int j = 0; j < NW; ++j)
+        for (int j = 0; j < NW; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = wc + 8 * j + 2 * t + e;
-          if (n >= a.NC) continue;
-          double* q = a.C + (cro[h] + ccs[n]);
-          double v = a.alpha * acc[j][2 * h + e];
-          if (a.beta != 0.0) v = fma(a.beta, *q, v);
-          *q = v;
-        }
+          for (int e = 0; e < 2; ++e)
+            a.C[cro[h] + ccs[wc + 8 * j + 2 * t + e]] = a.alpha * acc[j][2 * h + e];
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (cr0 + 8 * h >= a.R) continue;
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = wc + 8 * j + 2 * t + e;
+            if (n >= a.NC) continue;
+            double* q = a.C + (cro[h] + ccs[n]);
+            double v = a.alpha * acc[j][2 * h + e];
+            if (a.beta != 0.0) v = fma(a.beta, *q, v);
+            *q = v;
+          }
+      }
     }
     __syncthreads();   // the buffer of block `it` is refilled at iteration it + 1
   }
