@@ -870,7 +870,17 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       cp_async_wait_all();
       __syncwarp();
       const bool read_c = accumulate || beta != 0.0;
-      if (!c_lanes_n) {
+      if (!c_lanes_n && !read_c && m0 + BM <= M && n0 + BN <= N) {
+        // interior, write-only: no checks
+        const IDX rca = wtab[lane], rcb = wtab[lane + 32];
+#pragma unroll 8
+        for (int j = 0; j < WN; ++j) {
+          const IDX c = wtab[WM + j];
+          const float* src = epi + j * kEpiLD;
+          store_c(C + (rca + c), static_cast<T>(alpha * static_cast<double>(src[lane])), keep_c);
+          store_c(C + (rcb + c), static_cast<T>(alpha * static_cast<double>(src[lane + 32])), keep_c);
+        }
+      } else if (!c_lanes_n) {
         const int ma = m0 + mk.wm + lane, mb = ma + 32;
         const IDX rca = wtab[lane], rcb = wtab[lane + 32];
         const bool ina = ma < M, inb = mb < M;
