@@ -79,13 +79,16 @@ int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tenso
 /* Same operation on HOST buffers (the end-to-end path). Copies the address spans of A and B
  * (and of C when beta != 0, or when C's span has holes) to device staging memory, contracts,
  * copies C's span back, and synchronises `stream` before returning. The work is cut into up
- * to 8 chunks along one free label of C (the one with C's largest stride whose chunks are
+ * to 8 chunks along one free label x of C (the one with C's largest stride whose chunks are
  * disjoint address intervals and which adds at most 5% copy volume), so host->device copies,
- * kernels and device->host copies of consecutive chunks overlap on three streams; otherwise a
- * single chunk. Pinned host memory gives full copy bandwidth and overlap; pageable memory
- * works. Elements of C's span that are not elements of C are preserved. The staging memory
- * (the spans of A, B, C) is kept per device between calls; tc_release_staging() frees it.
- * Calls on one device are serialised by an internal lock. */
+ * kernels and device->host copies of consecutive chunks overlap on three streams. The operand
+ * without x (needed by every chunk) is uploaded first, or, when it has a bound label whose
+ * chunks are contiguous, streamed in up to 8 pieces behind the first chunk's kernels (that
+ * chunk is then summed over the pieces: beta on the first, 1 after). Otherwise one chunk.
+ * Pinned host memory gives full copy bandwidth and overlap; pageable memory works. Elements of
+ * C's span that are not elements of C are preserved. The staging memory (the spans of A, B, C)
+ * is kept per device between calls; tc_release_staging() frees it. Calls on one device are
+ * serialised by an internal lock. */
 int tc_contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                      double beta, const tc_tensor* C, void* stream);
 

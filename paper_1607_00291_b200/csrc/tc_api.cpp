@@ -448,26 +448,62 @@ static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const
   // work already queued on `stream` (e.g. the producer of the host inputs) comes first
   if (e == cudaSuccess) e = cudaEventRecord(e_start, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st.h2d, e_start, 0);
-  // Y (the operand without x) in full, then X and C chunk by chunk
+  // Y (the operand without x) is needed by every chunk. When Y has a bound label y whose
+  // chunks are contiguous (its outermost stride), the first chunk is itself computed as a sum
+  // over up to 8 y-pieces (beta on the first piece, 1 after), so Y streams in behind that
+  // chunk's kernels instead of being uploaded before the first one; otherwise Y goes up first.
   const int yt = best_c < 0 ? -1 : 1 - best_t;
-  if (e == cudaSuccess && yt >= 0) e = h2d(yt, whole[yt]);
+  int py = -1, pxy = -1;
+  int64_t ylen = 0, yq = 0;
+  if (yt >= 0) {
+    const tc_tensor* Y = T[yt];
+    for (int d = 0; d < Y->rank && py < 0; ++d) {
+      const int px = label_pos(T[best_t], Y->labels[d]);
+      if (px >= 0 && Y->lens[d] >= 2 && outer_dim(Y, d)) { py = d; pxy = px; }
+    }
+    if (py >= 0) { ylen = Y->lens[py]; yq = (ylen + kHostChunks - 1) / kHostChunks; }
+  }
+  const int nyp = py < 0 ? 0 : (int)((ylen + yq - 1) / yq);
+  std::vector<cudaEvent_t> e_ypc((size_t)nyp, nullptr);
+  for (int j = 0; j < nyp && e == cudaSuccess; ++j) e = event(&e_ypc[(size_t)j]);
+  if (e == cudaSuccess && yt >= 0 && py < 0) e = h2d(yt, whole[yt]);
   if (e == cudaSuccess) e = cudaEventRecord(e_y, st.h2d);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(s, e_y, 0);
-  for (int i = 0; i < nch && e == cudaSuccess && rc == TC_OK; ++i) {
-    const int64_t x0 = i * best_q, l = best_c < 0 ? 0 : std::min(best_q, best_len - x0);
-    // the chunk as tensors: x restricted to [x0, x0 + l)
+
+  // the sub-contraction with x in [x0, x0 + l) and (ly > 0) y in [y0, y0 + ly)
+  auto run = [&](int64_t x0, int64_t l, int64_t y0, int64_t ly, double beta_eff) {
     int64_t lens[3][TC_MAX_RANK];
     tc_tensor sub[3];
-    Piece pp[3];
     int64_t off[3] = {0, 0, 0};
     for (int t = 0; t < 3; ++t) {
       sub[t] = *T[t];
       for (int d = 0; d < T[t]->rank; ++d) lens[t][d] = T[t]->lens[d];
       sub[t].lens = lens[t];
       const int pos = best_c < 0 ? -1 : (t == 2 ? best_c : (t == best_t ? best_x : -1));
-      if (pos >= 0) { lens[t][pos] = l; off[t] = x0 * T[t]->strides[pos]; }
+      if (pos >= 0) { lens[t][pos] = l; off[t] += x0 * T[t]->strides[pos]; }
+      const int ypos = ly <= 0 ? -1 : (t == yt ? py : (t == best_t ? pxy : -1));
+      if (ypos >= 0) { lens[t][ypos] = ly; off[t] += y0 * T[t]->strides[ypos]; }
+    }
+    std::shared_ptr<Plan> p = full;
+    if (best_c >= 0) {
+      const int r = get_plan(dtype, &sub[0], &sub[1], &sub[2], &p);
+      if (r != TC_OK) return r;
+    }
+    const char* dp[3];
+    for (int t = 0; t < 3; ++t) dp[t] = dbase[t] ? dbase[t] + off[t] * (int64_t)esz : nullptr;
+    return execute(*p, alpha, dp[0], dp[1], beta_eff, const_cast<char*>(dp[2]), s);
+  };
+
+  for (int i = 0; i < nch && e == cudaSuccess && rc == TC_OK; ++i) {
+    const int64_t x0 = i * best_q, l = best_c < 0 ? 0 : std::min(best_q, best_len - x0);
+    // the chunk's address spans: x restricted to [x0, x0 + l)
+    Piece pp[3];
+    int64_t nCi = 1;
+    for (int t = 0; t < 3; ++t) {
+      const int pos = best_c < 0 ? -1 : (t == 2 ? best_c : (t == best_t ? best_x : -1));
       pp[t] = piece_of(T[t], pos, x0, l);
     }
+    for (int d = 0; d < C->rank; ++d) nCi *= d == best_c ? l : C->lens[d];
     if (best_c < 0) {
       if (need_ab) {
         if ((e = h2d(0, pp[0])) != cudaSuccess || (e = h2d(1, pp[1])) != cudaSuccess) break;
@@ -475,16 +511,21 @@ static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const
     } else if ((e = h2d(best_t, pp[best_t])) != cudaSuccess) {
       break;
     }
-    int64_t nCi = 1;
-    for (int d = 0; d < C->rank; ++d) nCi *= lens[2][d];
     if (c_upload(pp[2], nCi) && (e = h2d(2, pp[2])) != cudaSuccess) break;
     if ((e = cudaEventRecord(e_in[(size_t)i], st.h2d)) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(s, e_in[(size_t)i], 0)) != cudaSuccess) break;
-    std::shared_ptr<Plan> p = full;
-    if (best_c >= 0 && (rc = get_plan(dtype, &sub[0], &sub[1], &sub[2], &p)) != TC_OK) break;
-    const char* dp[3];
-    for (int t = 0; t < 3; ++t) dp[t] = dbase[t] ? dbase[t] + off[t] * (int64_t)esz : nullptr;
-    if ((rc = execute(*p, alpha, dp[0], dp[1], beta, const_cast<char*>(dp[2]), s)) != TC_OK) break;
+    if (i == 0 && nyp > 0) {
+      for (int j = 0; j < nyp && e == cudaSuccess && rc == TC_OK; ++j) {
+        const int64_t y0 = j * yq, ly = std::min(yq, ylen - y0);
+        if ((e = h2d(yt, piece_of(T[yt], py, y0, ly))) != cudaSuccess) break;
+        if ((e = cudaEventRecord(e_ypc[(size_t)j], st.h2d)) != cudaSuccess) break;
+        if ((e = cudaStreamWaitEvent(s, e_ypc[(size_t)j], 0)) != cudaSuccess) break;
+        rc = run(x0, l, y0, ly, j == 0 ? beta : 1.0);
+      }
+      if (e != cudaSuccess || rc != TC_OK) break;
+    } else if ((rc = run(x0, l, 0, 0, beta)) != TC_OK) {
+      break;
+    }
     if ((e = cudaEventRecord(e_out[(size_t)i], s)) != cudaSuccess) break;
     if ((e = cudaStreamWaitEvent(st.d2h, e_out[(size_t)i], 0)) != cudaSuccess) break;
     if (pp[2].lo <= pp[2].hi)
