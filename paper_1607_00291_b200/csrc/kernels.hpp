@@ -35,7 +35,8 @@ struct LaunchArgs {
   bool a_elem, b_elem;
   bool f32_a_transpose;
   bool c_lanes_n;
-  int skinny_bu, skinny_bv;   // skinny kernel: X rows come in bv runs of bu (plan.cpp)        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
+  int skinny_bu, skinny_bv;
+  int tiny_mn_log2, tiny_mnk_log2;   // tiny.cu applies up to 2^mn elements of C, 2^mnk FMAs   // skinny kernel: X rows come in bv runs of bu (plan.cpp)        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA
@@ -50,8 +51,8 @@ struct LaunchArgs {
 // `force`: also when the streamed operand is not contiguous along its rows.
 int launch_skinny(const LaunchArgs& a, cudaStream_t stream, bool force);
 
-// Tiny contractions (<= 2^21 multiply-adds, <= 2^16 elements of C): tiny.cu, one thread per
-// element of C. 0 = not applicable, 1 = launched, -1 = CUDA error.
+// Tiny contractions (<= 2^24 multiply-adds, <= 2^18 elements of C, K <= 256): tiny.cu, one
+// thread per element of C. 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_tiny(const LaunchArgs& a, cudaStream_t stream);
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).

@@ -154,6 +154,19 @@ static int gather_override() {
   return g;
 }
 
+// Size limits of the tiny-contraction kernel (log2 of C elements and of multiply-adds);
+// TC_TINY_LIMITS="mn,mnk" overrides them (tuning experiments).
+static void tiny_limits(int* mn, int* mnk) {
+  static int lim[2] = {-1, -1};
+  if (lim[0] < 0) {
+    lim[0] = 18; lim[1] = 24;
+    const char* e = getenv("TC_TINY_LIMITS");
+    if (e) std::sscanf(e, "%d,%d", &lim[0], &lim[1]);
+  }
+  *mn = lim[0];
+  *mnk = lim[1];
+}
+
 static bool f32_a_transpose() {
   static const bool f = [] {
     const char* e = getenv("TC_FFMA_AT");
@@ -225,6 +238,7 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.f32_a_transpose = f32_a_transpose() && !force_scatter();
   a.c_lanes_n = p.c_unit_n;
   a.skinny_bu = p.skinny_bu;
+  tiny_limits(&a.tiny_mn_log2, &a.tiny_mnk_log2);
   a.skinny_bv = p.skinny_bv;
   a.num_sms = d->num_sms;
   a.flags_cap = 2 * d->num_sms;

@@ -4,8 +4,7 @@
 // computes one element of C directly from the definition through the scatter vectors
 // (P:541-546): C[rC[m] + cC[n]] = alpha * sum_k A[rA[m] + cA[k]] * B[rB[k] + cB[n]] + beta * C,
 // with an fp64 accumulator (rounded once for fp32, reading R12), spread over enough CTAs that
-// the call costs little more than a launch. Threads run along M so that C's unit-stride
-// bundle (put first by the heuristic) is written by consecutive lanes.
+// the call costs little more than a launch.
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -15,38 +14,55 @@
 namespace tcb {
 namespace tiny {
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;   // consecutive m (C's unit-stride bundle)
+constexpr int kNB = 4;          // columns of C per thread (B values shared through smem)
+constexpr int kMaxK = 256;
 
+// CTA = 128 consecutive rows x kNB columns of C. The CTA first stages A's K offsets and its
+// kNB columns of B (K x kNB values) in shared memory, so the K loop issues one independent
+// global load per k (A, coalesced along M when A is) instead of two dependent table lookups
+// and two operand loads; each A value feeds kNB multiply-adds.
 template <typename T, typename IDX>
 __global__ void __launch_bounds__(kThreads) tc_tiny_kernel(
     const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
     const IDX* __restrict__ rA, const IDX* __restrict__ cA, const IDX* __restrict__ rB,
     const IDX* __restrict__ cB, const IDX* __restrict__ rC, const IDX* __restrict__ cC, int M,
     int N, int K, double alpha, double beta) {
-  const long long e = (long long)blockIdx.x * kThreads + threadIdx.x;
-  if (e >= (long long)M * N) return;
-  const int m = (int)(e % M), n = (int)(e / M);
-  const IDX ra = rA[m], cb = cB[n];
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;   // four partial sums: independent FMAs
-  int k = 0;
-  for (; k + 4 <= K; k += 4) {
-    s0 = fma(static_cast<double>(A[ra + cA[k]]), static_cast<double>(B[rB[k] + cb]), s0);
-    s1 = fma(static_cast<double>(A[ra + cA[k + 1]]), static_cast<double>(B[rB[k + 1] + cb]), s1);
-    s2 = fma(static_cast<double>(A[ra + cA[k + 2]]), static_cast<double>(B[rB[k + 2] + cb]), s2);
-    s3 = fma(static_cast<double>(A[ra + cA[k + 3]]), static_cast<double>(B[rB[k + 3] + cb]), s3);
+  __shared__ IDX cas[kMaxK];
+  __shared__ double bs[kMaxK][kNB];
+  const int m = blockIdx.x * kThreads + threadIdx.x;
+  const int n0 = blockIdx.y * kNB;
+  for (int k = threadIdx.x; k < K; k += kThreads) cas[k] = cA[k];
+  for (int e = threadIdx.x; e < K * kNB; e += kThreads) {
+    const int k = e / kNB, j = e - k * kNB;
+    bs[k][j] = n0 + j < N ? static_cast<double>(B[rB[k] + cB[n0 + j]]) : 0.0;
   }
-  for (; k < K; ++k)
-    s0 = fma(static_cast<double>(A[ra + cA[k]]), static_cast<double>(B[rB[k] + cb]), s0);
-  T* q = C + (rC[m] + cC[n]);
-  double v = alpha * ((s0 + s1) + (s2 + s3));
-  if (beta != 0.0) v = fma(beta, static_cast<double>(*q), v);
-  *q = static_cast<T>(v);
+  __syncthreads();
+  if (m >= M) return;
+  const IDX ra = rA[m];
+  double acc[kNB];
+#pragma unroll
+  for (int j = 0; j < kNB; ++j) acc[j] = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < K; ++k) {
+    const double a = static_cast<double>(A[ra + cas[k]]);
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) acc[j] = fma(a, bs[k][j], acc[j]);
+  }
+  const IDX rc = rC[m];
+#pragma unroll
+  for (int j = 0; j < kNB; ++j) {
+    if (n0 + j >= N) break;
+    T* q = C + (rc + cC[n0 + j]);
+    double v = alpha * acc[j];
+    if (beta != 0.0) v = fma(beta, static_cast<double>(*q), v);
+    *q = static_cast<T>(v);
+  }
 }
 
 template <typename T, typename IDX>
 static int launch_t(const LaunchArgs& a, cudaStream_t s) {
-  const long long n = (long long)a.M * a.N;
-  const int grid = (int)((n + kThreads - 1) / kThreads);
+  const dim3 grid((a.M + kThreads - 1) / kThreads, (a.N + kNB - 1) / kNB);
   tc_tiny_kernel<T, IDX><<<grid, kThreads, 0, s>>>(
       static_cast<const T*>(a.A), static_cast<const T*>(a.B), static_cast<T*>(a.C),
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
@@ -58,11 +74,15 @@ static int launch_t(const LaunchArgs& a, cudaStream_t s) {
 
 }  // namespace tiny
 
-// Applies when the whole contraction is at most 2^21 multiply-adds over at most 2^16 elements
-// of C (cfg1 is 2^18 over 2^12). 0 = not applicable, 1 = launched, -1 = CUDA error.
+// Applies when the contraction has at most 2^18 elements of C, at most 2^24 multiply-adds and
+// K <= 256 (cfg1 is 2^12 / 2^18 / 64): there it beats the tensor-core tile kernel, whose few
+// tiles run on few SMs (profiles/r01/tiny_sweep.jsonl, kernel time in CUDA graphs).
+// 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_tiny(const LaunchArgs& a, cudaStream_t stream) {
   const long long mn = (long long)a.M * a.N;
-  if (mn > (1ll << 16) || mn * (a.K > 0 ? a.K : 1) > (1ll << 21)) return 0;
+  if (a.K > tiny::kMaxK || a.N > 65535 * tiny::kNB || mn > (1ll << a.tiny_mn_log2) ||
+      mn * (a.K > 0 ? a.K : 1) > (1ll << a.tiny_mnk_log2))
+    return 0;
   if (a.f32)
     return a.idx64 ? tiny::launch_t<float, long long>(a, stream)
                    : tiny::launch_t<float, int>(a, stream);
