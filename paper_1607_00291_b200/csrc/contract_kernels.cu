@@ -386,6 +386,12 @@ static bool tiny_enabled() {
   return !(e && !strcmp(e, "0"));
 }
 
+// TC_F32_UMMA=1 sends fp32 contractions to the tcgen05 3xTF32 kernel (umma_f32.cu).
+static bool umma_f32_enabled() {
+  const char* e = getenv("TC_F32_UMMA");
+  return e && !strcmp(e, "1");
+}
+
 int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (args.M <= 0 || args.N <= 0) return 0;
   const int choice = kernel_choice();
@@ -399,6 +405,10 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   }
   if (choice == 1 && !args.f32)
     return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
+  if (choice == 0 && args.f32 && umma_f32_enabled()) {
+    const int r = launch_umma_f32(args, stream);
+    if (r != 0) return r;
+  }
   LaunchArgs a = args;
   a.stream_k = choice != 2;
   return launch_ws(a, stream);

@@ -31,6 +31,14 @@ def tc():
     return m
 
 
+@pytest.fixture(params=["0", "1"], ids=["ffma", "umma"])
+def both_f32_paths(request, monkeypatch):
+    """fp32 cases through the FFMA2 kernel and, with TC_F32_UMMA=1, the tcgen05 3xTF32 kernel
+    (umma_f32.cu); the library reads TC_F32_UMMA on every call."""
+    monkeypatch.setenv("TC_F32_UMMA", request.param)
+    return request.param
+
+
 @pytest.fixture(params=["1", "0"], ids=["tiny", "tensorcore"])
 def both_small_paths(request, monkeypatch):
     """Small cases run through the tiny kernel (tiny.cu) and, with TC_TINY=0, through the
@@ -389,11 +397,13 @@ def test_repeat_calls_bitwise_deterministic():
 # fp32 (cfg4's fp32 half): operands widened to fp64 in the micro-kernel, rounded once (R12)
 # ---------------------------------------------------------------------------------------------
 
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.parametrize("i", range(20))
 def test_cfg4_scaled_f32(i):
     check(_scaled_cfg4(i, torch.float32))
 
 
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.parametrize("i", range(20))
 def test_cfg4_full_sampled_f32(i):
     case = W.cfg4(i, torch.float32)
@@ -405,6 +415,7 @@ def test_cfg4_full_sampled_f32(i):
     assert e < TOL[torch.float32]
 
 
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.parametrize("spec", ["mn-mk-kn", "mn-km-nk", "mn-mk-nk", "mn-km-kn"])
 @pytest.mark.parametrize("mnk", [(203, 145, 171), (256, 128, 64)])
 def test_f32_loader_directions(spec, mnk):
@@ -423,6 +434,7 @@ def test_random_small_f32(seed):
     check(W.random_tiny_case(seed, max_rank=6, max_len=7, dtype=torch.float32))
 
 
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.usefixtures("both_small_paths")
 def test_f32_misaligned_views():
     g = torch.Generator().manual_seed(4)

@@ -27,9 +27,11 @@ __device__ __forceinline__ uint64_t make_desc(const void* smem, uint32_t lbo, ui
   return d;                  // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
 }
 
-// element (r, k) of a 128 x 32 tile, in floats
-__device__ __forceinline__ int kmajor_off(int r, int k) {
-  return (k >> 2) * (R * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
+// element (r, k) of a 128 x 32 tile, in floats: K-major or MN-major canonical layout
+template <bool MN>
+__device__ __forceinline__ int tile_off(int r, int k) {
+  return MN ? (k >> 3) * 1024 + (r >> 2) * 32 + (k & 7) * 4 + (r & 3)
+            : (k >> 2) * (R * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
 }
 
 __device__ __forceinline__ float tf32_hi(float x) {
@@ -38,8 +40,8 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(u);
 }
 
-template <bool THREE>
-__global__ void umma_test(const float* A, const float* B, float* D) {
+template <bool THREE, bool AMN, bool BMN>
+__global__ void umma_test(const float* A, const float* B, float* D, uint32_t lbo_mn, uint32_t sbo_mn) {
   extern __shared__ __align__(1024) float dsm[];
   float* sa = dsm;
   float* sb = sa + R * KS;
@@ -52,10 +54,10 @@ __global__ void umma_test(const float* A, const float* B, float* D) {
     const int r = e / KS, k = e % KS;
     const float a = A[r * KS + k], b = B[r * KS + k];
     const float ah = THREE ? tf32_hi(a) : a, bh = THREE ? tf32_hi(b) : b;
-    sa[kmajor_off(r, k)] = ah;
-    sb[kmajor_off(r, k)] = bh;
-    sal[kmajor_off(r, k)] = a - ah;
-    sbl[kmajor_off(r, k)] = b - bh;
+    sa[tile_off<AMN>(r, k)] = ah;
+    sb[tile_off<BMN>(r, k)] = bh;
+    sal[tile_off<AMN>(r, k)] = a - ah;
+    sbl[tile_off<BMN>(r, k)] = b - bh;
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;\n"
@@ -70,7 +72,8 @@ __global__ void umma_test(const float* A, const float* B, float* D) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = tmem_base;
-  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(R >> 3) << 17) |
+  const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) |
+                         ((BMN ? 1u : 0u) << 16) | ((uint32_t)(R >> 3) << 17) |
                          ((uint32_t)(R >> 4) << 24);
   if (tid == 0) {
     const uint32_t LBO = R * 16, SBO = 128;
@@ -79,7 +82,8 @@ __global__ void umma_test(const float* A, const float* B, float* D) {
       const float* ap[3] = {sa, sa, sal};
       const float* bp[3] = {sb, sbl, sb};
       for (int q = 0; q < (THREE ? 3 : 1); ++q) {
-        const uint64_t da = make_desc(ap[q] + off, LBO, SBO), db = make_desc(bp[q] + off, LBO, SBO);
+        const uint64_t da = AMN ? make_desc(ap[q] + off, lbo_mn, sbo_mn) : make_desc(ap[q] + off, LBO, SBO);
+        const uint64_t db = BMN ? make_desc(bp[q] + off, lbo_mn, sbo_mn) : make_desc(bp[q] + off, LBO, SBO);
         const uint32_t acc = (j > 0 || q > 0) ? 1u : 0u;
         asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
@@ -123,27 +127,30 @@ int main() {
   cudaMalloc(&dA, A.size() * 4); cudaMalloc(&dB, B.size() * 4); cudaMalloc(&dD, D.size() * 4);
   cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
-  for (int three = 0; three < 2; ++three) {
+  const int smem = 4 * R * KS * 4;
+  auto run = [&](auto kern, const char* name, uint32_t lbo, uint32_t sbo) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaMemset(dD, 0, D.size() * 4);
-    const int smem = 4 * R * KS * 4;
-    cudaFuncSetAttribute(umma_test<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(umma_test<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (three) umma_test<true><<<1, 128, smem>>>(dA, dB, dD);
-    else umma_test<false><<<1, 128, smem>>>(dA, dB, dD);
+    kern<<<1, 128, smem>>>(dA, dB, dD, lbo, sbo);
     cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
+    if (e != cudaSuccess) { printf("%s: CUDA error %s\n", name, cudaGetErrorString(e)); exit(1); }
     cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost);
-    double num = 0, den = 0, maxd = 0;
+    double num = 0, den = 0;
     for (int m = 0; m < R; ++m)
       for (int n = 0; n < R; ++n) {
         double s = 0;
         for (int k = 0; k < KS; ++k) s += (double)A[m * KS + k] * B[n * KS + k];
         num += (D[m * R + n] - s) * (D[m * R + n] - s);
         den += s * s;
-        maxd = fmax(maxd, fabs(D[m * R + n] - s));
       }
-    printf("%s: normwise rel err %.3e, max abs err %.3e, D[0]=%f D[last]=%f\n",
-           three ? "3xTF32" : "TF32  ", sqrt(num / den), maxd, D[0], D[R * R - 1]);
+    printf("%-28s lbo %5u sbo %5u: normwise rel err %.3e  D[0]=%f\n", name, lbo, sbo, sqrt(num / den), D[0]);
+  };
+  run(umma_test<false, false, false>, "TF32   K/K", 4096, 128);
+  run(umma_test<true, false, false>, "3xTF32 K/K", 4096, 128);
+  for (uint32_t lbo : {4096u, 128u}) for (uint32_t sbo : {128u, 4096u}) {
+    run(umma_test<true, true, false>, "3xTF32 MN/K", lbo, sbo);
+    run(umma_test<true, false, true>, "3xTF32 K/MN", lbo, sbo);
+    run(umma_test<true, true, true>, "3xTF32 MN/MN", lbo, sbo);
   }
   return 0;
 }
