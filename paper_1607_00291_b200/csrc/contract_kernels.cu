@@ -386,10 +386,12 @@ static bool tiny_enabled() {
   return !(e && !strcmp(e, "0"));
 }
 
-// TC_F32_UMMA=1 sends fp32 contractions to the tcgen05 3xTF32 kernel (umma_f32.cu).
+// fp32 contractions run on the tcgen05 tensor cores as 3xTF32 (umma_f32.cu): 1.1-1.6x SGEMM on
+// cfg4 against 0.7-0.95x for the FFMA2 kernel (profiles/r01/ab_f32_umma.txt). TC_F32_UMMA=0
+// selects the FFMA2 kernel (contract_ws.cuh) instead. Read on every call (tests cover both).
 static bool umma_f32_enabled() {
   const char* e = getenv("TC_F32_UMMA");
-  return e && !strcmp(e, "1");
+  return !(e && !strcmp(e, "0"));
 }
 
 int launch_contract(const LaunchArgs& args, cudaStream_t stream) {

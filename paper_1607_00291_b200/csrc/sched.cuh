@@ -1,0 +1,105 @@
+// Persistent tile schedule shared by the tensor-core kernels (contract_ws.cuh, umma_f32.cu):
+// data-parallel whole tiles plus a stream-K tail fixed up in place through per-tile flags.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tcb {
+namespace sched {
+
+// ------------------------------------------------------------------------------------------
+// Persistent schedule: data-parallel full waves + a stream-K tail.
+// Tiles [0, D) are whole tiles, dealt round-robin (CTA w takes w, w+P, ...), so CTAs running at
+// the same time work on consecutive tiles (L2 reuse through the grouped rasterisation). The
+// last S = T - D tiles are split by K iterations evenly over P_sk CTAs (stream-K), which removes
+// the wave-quantisation loss of the final partial wave. Each CTA walks its stream-K range in
+// REVERSE tile order, so the k-first piece of every split tile is computed at the start of the
+// tail and its k-last piece at the end: the first piece writes alpha*acc + beta*C, later pieces
+// add alpha*acc in a fixed order behind a per-tile flag. No partial-sum workspace, deterministic
+// results, and a piece only waits on lower-ranked CTAs' first work items (no deadlock).
+// ------------------------------------------------------------------------------------------
+struct Sched {
+  int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
+  int P_sk;                 // CTAs in the stream-K tail (0: no tail)
+  long long I;              // stream-K iterations = (T - D) * KT
+  // wave alignment of the data-parallel phase: before its j-th whole tile (j >= 1) a CTA's
+  // producers wait (bounded) until the wave counter reaches wave_base + j * P, i.e. every CTA
+  // has issued its loads of wave j - 1, so the CTAs of a wave walk K together and share the A
+  // and B panels in L2 instead of drifting apart over hundreds of waves
+  unsigned wave_base;
+  int wave_sync;
+};
+
+struct WorkIter {
+  int dp_t, D, P, KT;
+  int sk_t, sk_lo;          // current / lowest stream-K tile (relative to D), descending
+  long long g0, g1;         // this CTA's stream-K iteration range
+
+  __device__ __forceinline__ void init(const Sched& s, int w) {
+    D = s.D; P = s.P; KT = s.KT;
+    dp_t = w < s.P ? w : s.D;
+    sk_t = -1; sk_lo = 0; g0 = g1 = 0;
+    if (w < s.P_sk) {
+      g0 = (long long)w * s.I / s.P_sk;
+      g1 = (long long)(w + 1) * s.I / s.P_sk;
+      if (g1 > g0) { sk_t = (int)((g1 - 1) / KT); sk_lo = (int)(g0 / KT); }
+    }
+  }
+  // next work item: tile index, K-iteration range [kb, ke), stream-K piece flag
+  __device__ __forceinline__ bool next(int& tile, int& kb, int& ke, bool& sk) {
+    if (dp_t < D) { tile = dp_t; dp_t += P; kb = 0; ke = KT; sk = false; return true; }
+    if (sk_t >= sk_lo) {
+      const long long base = (long long)sk_t * KT;
+      kb = (int)(g0 > base ? g0 - base : 0);
+      ke = (int)(g1 - base < KT ? g1 - base : KT);
+      tile = D + sk_t;
+      --sk_t;
+      sk = true;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Host side of the schedule: D whole tiles round-robin over P = #SMs CTAs, the rest split by
+// K iterations over P_sk CTAs (each gets >= kMinSkIters iterations). TC_KERNEL=ws_nosk turns
+// the tail off (all tiles data-parallel) for ablation.
+constexpr int kMinSkIters = 8;
+constexpr int kMaxPieces = 16;   // at most this many stream-K pieces per tile (fix-up chain)
+
+inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88) {
+  Sched s{};
+  s.T = T; s.KT = KT; s.P = nsm;
+  // Which tiles are split: the last full wave and the partial wave (stream-K over 1-2 waves,
+  // enough iterations per CTA for a short tail), unless the partial wave is >= 88% full, which
+  // then runs data-parallel (its idle share is smaller than the cost of the split pieces'
+  // extra epilogues). Measured on cfg4 (profiles/r01/ab_sk_policy.txt); the fp32 tcgen05
+  // kernel passes dp_pct = 70 (profiles/r01/ab_umma_sk.txt).
+  int D;
+  const int rem = T % nsm;
+  if (!allow_sk || KT == 0 || rem == 0 || rem * 100 >= dp_pct * nsm) D = T;
+  else if (T < nsm) D = 0;
+  else D = (T / nsm - 1) * nsm;
+  s.D = D;
+  s.I = (long long)(T - D) * KT;
+  long long psk = s.I / kMinSkIters;   // each stream-K CTA gets >= kMinSkIters iterations
+  if (psk < 1) psk = 1;
+  if (psk > nsm) psk = nsm;
+  if (psk > (long long)(T - D) * kMaxPieces) psk = (long long)(T - D) * kMaxPieces;
+  s.P_sk = D < T ? (int)psk : 0;
+  return s;
+}
+
+}  // namespace sched
+}  // namespace tcb

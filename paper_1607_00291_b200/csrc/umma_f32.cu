@@ -1,64 +1,79 @@
 // fp32 contraction on the 5th-generation tensor cores (sm_100a tcgen05, kind::tf32) with the
 // 3xTF32 split: every fp32 operand x is split into hi = tf32(x) and lo = x - hi, and
-// A.B = Ahi.Bhi + Ahi.Blo + Alo.Bhi (the Alo.Blo term, ~2^-22 relative, is dropped), accumulated
-// in fp32 in tensor memory. The error stays at fp32 level (plain TF32 would be ~1e-3); the
-// normwise bound 1e-5 of BASELINE north_star is checked by the parity tests.
+// A.B = Ahi.Bhi + Ahi.Blo + Alo.Bhi (the Alo.Blo term, ~2^-20 relative, is dropped), accumulated
+// in fp32 in tensor memory (reading R18 in DESIGN.md). Normwise error ~1e-6 on cfg4 (FFMA2
+// kernel: 0.7-1.1e-6), against the 1e-5 bound of BASELINE north_star checked by the parity tests.
 //
 // The paper's method is unchanged: the tiles are gathered from the tensors' strides through the
 // scatter vectors -- here straight into the tensor cores' canonical
 // shared-memory layout -- and C is written through its scatter vectors with alpha / beta
-// (P:605-616). One CTA per SM walks 128 x 128 tiles of C:
+// (P:605-616). One CTA per SM walks the persistent schedule of sched.cuh (whole 128 x 128 tiles
+// of C, then stream-K pieces fixed up in place):
 //   warps 0-3   producers: cp.async element gathers of A and B (128 x 32 each per K step) into
 //               the stage's hi buffers in the K-major canonical layout; each warp instruction
 //               fills one 128-byte core matrix (8 rows x 4 K), so shared-memory writes are
 //               conflict free and global reads come in 32-byte runs from an M/N-contiguous
 //               operand (8 rows) or 16-byte runs from a K-contiguous one (4 K)
-//   warps 4-7   converters: split each staged element into hi (in place) and lo (second buffer)
-//   warps 8-11  epilogue: tcgen05.ld of the accumulator (warp w reads TMEM lanes 32 (w - 8)..),
+//   warps 4-7   converters: hi stays the raw fp32 value (the tensor core reads its tf32 bits,
+//               i.e. truncates); lo = rna(x - trunc(x)) goes to the stage's lo buffers
+//   warps 8-11  epilogue: tcgen05.ld of each chunk accumulator (warp w reads TMEM lanes
+//               32 (w - 8)..), added into the running sum in TMEM; at the end of a work item
 //               one row of C per thread, alpha * acc + beta * C through rscat_C / cscat_C
 //   warp 12     MMA issuer: one lane issues 3 x 4 tcgen05.mma (M = N = 128, K = 8) per K step and
-//               commits them to the stage's `empty` barrier; two TMEM accumulators let the
-//               epilogue of tile t overlap the MMAs of tile t + 1.
+//               commits them to the stage's `empty` barrier; two TMEM chunk accumulators let
+//               the epilogue's adds overlap the next chunk's MMAs.
 #include <cstdint>
-#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include <cuda_runtime.h>
 
 #include "dev_common.cuh"
 #include "kernels.hpp"
+#include "sched.cuh"
 
 namespace tcb {
 namespace umma {
 
 using namespace dev;
+using namespace sched;
 
 constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
-constexpr int kThreads = 13 * 32;
-constexpr int kTile = BM * BK;           // floats per operand tile (BM == BN)
+#ifndef TC_UMMA_PW
+#define TC_UMMA_PW 4
+#endif
+constexpr int kPW = TC_UMMA_PW;            // producer warps (4 or 8)
+constexpr int kConv0 = kPW, kEpi0 = kPW + 4, kMmaW = kPW + 8;   // first warp of each role
+constexpr int kThreads = (kPW + 9) * 32;
+constexpr int kTile = (BK / 4) * (128 * 4 + 16);   // floats per operand tile (padded K chunks)
 constexpr int kStage = 4 * kTile;        // A hi, A lo, B hi, B lo
 constexpr int GROUP_M = 2;
-// The tensor core's fp32 accumulation drifts with the number of MMA steps it chains (3xTF32 at
-// K = 513: 3.7e-6 normwise, growing with K), so the accumulator restarts every kChunkSteps K
-// steps; the epilogue warps add the chunk into a running sum held in TMEM (rounded fp32 adds).
-constexpr int kChunkSteps = 4;             // K steps of BK per chunk (K = 128)
+// The tensor core's fp32 accumulation is biased (it truncates): on one-signed data the relative
+// error grows with the number of MMAs chained into one accumulator (3xTF32, K = 128 per
+// accumulator: -2.6e-6 bias; K = 32: -7.6e-7), so the accumulator restarts every kChunkSteps K
+// steps and the epilogue warps add each chunk into a running sum held in TMEM (rounded fp32
+// adds, like an FFMA loop). One K step per chunk costs ~2% against four
+// (profiles/r01/ab_umma_chunk.txt).
+#ifndef TC_UMMA_CHUNK
+#define TC_UMMA_CHUNK 1
+#endif
+constexpr int kChunkSteps = TC_UMMA_CHUNK;   // K steps of BK per chunk
 
 __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u32(p); }
 
-// Canonical SWIZZLE_NONE layouts (CUTLASS UMMA conventions, in floats):
-//  K-major : core matrix = 8 rows x 4 K (16 B per row); row groups of 8 at 32 floats (SBO 128 B),
-//            K chunks of 4 at 512 floats (LBO 2 KB); one K = 8 MMA step spans two K chunks
-//  MN-major: core matrix = 8 K x 4 rows (16 B per K); row groups of 4 at 32 floats (SBO 128 B),
-//            K groups of 8 at 1024 floats (LBO 4 KB); one MMA step is one K group
-template <bool MN>
+// Canonical SWIZZLE_NONE K-major layout (in floats): core matrix = 8 rows x 4 K (16 B per row);
+// row groups of 8 at 32 floats (SBO 128 B), K chunks of 4 at kChunk floats (LBO); one K = 8 MMA
+// step spans two K chunks. kChunk = 512 + 16: the 64-byte pad puts the two K chunks a K-run
+// gather writes in one instruction on different banks. (The MN-major tf32 operand mode left the
+// accumulator at zero on this part, tools/calib/umma_tf32_test.cu, so both operands are K-major.)
+constexpr int kChunk = 128 * 4 + 16;
 __device__ __forceinline__ int tile_off(int r, int k) {
-  return MN ? (k >> 3) * 1024 + (r >> 2) * 32 + (k & 7) * 4 + (r & 3)
-            : (k >> 2) * 512 + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
+  return (k >> 2) * kChunk + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
 }
 
-template <bool MN>
 __device__ __forceinline__ uint64_t make_desc(const float* base, int j) {   // MMA step j (K 8j..)
-  const uint32_t addr = smem_u32(base + j * 1024);
-  const uint32_t lbo = MN ? 4096 : 2048, sbo = 128;
+  const uint32_t addr = smem_u32(base + j * 2 * kChunk);
+  const uint32_t lbo = kChunk * 4, sbo = 128;
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
@@ -98,58 +113,80 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&u)[32
          "r"(u[27]), "r"(u[28]), "r"(u[29]), "r"(u[30]), "r"(u[31])
       : "memory");
 }
+#ifndef TC_UMMA_HI_TRUNC
+#define TC_UMMA_HI_TRUNC 1
+#endif
+__device__ __forceinline__ float tf32_trunc(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t u;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
   return __uint_as_float(u);
 }
 
-// Producer side of one operand X (A: rows = M, B: rows = N). MN: gathered along its rows.
-// Warp w covers a quarter of the tile's core matrices; lane l is element (l & 3 | l >> 2) of
-// each core matrix it copies.
-template <typename IDX, bool MN>
+// Producer side of one operand X (A: rows = M, B: rows = N), 4-byte cp.async element gathers
+// laid out so that a warp instruction touches as few 32-byte sectors as the operand allows:
+//  KR = false (X contiguous along its rows): lanes = 8 rows x 4 K, one core matrix per
+//             instruction, 32-byte runs along the rows
+//  KR = true  (X contiguous along K): lanes = 4 rows x 8 K, 32-byte runs along K (two core
+//             matrices half-filled, on disjoint banks thanks to the K-chunk pad)
+// Either way 4 sectors per 128 bytes when the operand is contiguous (a K-run operand read with
+// the row mapping would touch 8).
+template <typename IDX, bool KR>
 struct Gather {
-  static constexpr int NR = MN ? 8 : 4;    // row groups per warp (of 4 or 8 rows)
-  static constexpr int NK = MN ? 4 : 8;    // K groups per stage (of 8 or 4)
+  static constexpr int RG = KR ? 4 : 8;               // rows per instruction
+  static constexpr int KG = KR ? 8 : 4;               // K per instruction
+  static constexpr int NR = 128 / RG / kPW;           // row groups per warp
+  static constexpr int NK = BK / KG;                  // K groups per stage
   IDX ro[NR];
   uint32_t rv;
   IDX ko[NK];
+  __device__ __forceinline__ static int row(int w, int i, int l) {
+    return RG * (w * NR + i) + (KR ? (l >> 3) : (l >> 2));
+  }
+  __device__ __forceinline__ static int kin_(int j, int l) {
+    return KG * j + (KR ? (l & 7) : (l & 3));
+  }
   __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
                                        int l) {
     rv = 0;
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
-      const int r = base + (MN ? 4 * (w * NR + i) + (l & 3) : 8 * (w * NR + i) + (l >> 2));
+      const int r = base + row(w, i, l);
       ro[i] = rtab[r];                       // tables are padded past the extent
       rv |= (r < extent ? 1u : 0u) << i;
     }
   }
   __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
 #pragma unroll
-    for (int j = 0; j < NK; ++j) ko[j] = __ldg(ktab + k0 + (MN ? 8 * j + (l >> 2) : 4 * j + (l & 3)));
+    for (int j = 0; j < NK; ++j) ko[j] = __ldg(ktab + k0 + kin_(j, l));
   }
   __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
                                         int l) {
 #pragma unroll
     for (int j = 0; j < NK; ++j) {
-      const int kk = MN ? 8 * j + (l >> 2) : 4 * j + (l & 3);
+      const int kk = kin_(j, l);
       const bool kin = k0 + kk < K;
 #pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        const int r = MN ? 4 * (w * NR + i) + (l & 3) : 8 * (w * NR + i) + (l >> 2);
-        cp_async4(sm + tile_off<MN>(r, kk), g + (ro[i] + ko[j]), kin && ((rv >> i) & 1u));
-      }
+      for (int i = 0; i < NR; ++i)
+        cp_async4(sm + tile_off(row(w, i, l), kk), g + (ro[i] + ko[j]), kin && ((rv >> i) & 1u));
     }
   }
 };
 
-template <typename IDX, bool A_MN, bool B_MN>
+__device__ __forceinline__ void epi_sync() {   // the four epilogue warps only
+  asm volatile("bar.sync 1, 128;\n" ::: "memory");
+}
+
+template <typename IDX, bool A_KR, bool B_KR>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
                    const IDX* __restrict__ rA, const IDX* __restrict__ cA,
                    const IDX* __restrict__ rB, const IDX* __restrict__ cB,
                    const IDX* __restrict__ rC, const IDX* __restrict__ cC, int M, int N, int K,
-                   int tiles_m, int tiles_n, double alpha, double beta) {
+                   int tiles_m, int tiles_n, double alpha, double beta, Sched sched,
+                   int* __restrict__ flags) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* stage0 = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * kStage * sizeof(float));
@@ -162,7 +199,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 128);
+      mbar_init(&full[s], kPW * 32);
       mbar_init(&conv[s], 128);
       mbar_init(&empty[s], 1);
     }
@@ -172,7 +209,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 12) {
+  if (warp == kMmaW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
                  :: "r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -182,37 +219,51 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  const int T = tiles_m * tiles_n;
-  const int KT = (K + BK - 1) / BK;
+  // every role walks the same work items: whole tiles, then this CTA's stream-K pieces
+  // (sched.cuh); a piece is the K-step range [kb, ke) of one tile
+  WorkIter wi;
+  wi.init(sched, blockIdx.x);
+  int tile, kb, ke;
+  bool sk;
 
-  if (warp < 4) {
+  if (warp < kPW) {
     // ---------------------------------- producers ----------------------------------
-    Gather<IDX, A_MN> ga;
-    Gather<IDX, B_MN> gb;
+    Gather<IDX, A_KR> ga;
+    Gather<IDX, B_KR> gb;
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    // K offsets depend on the K step only: those of the next step are fetched while this one's
+    // copies are in flight, so the table reads stay off the producer's critical path
+    int kpre = 0;
+    ga.load_k(cA, 0, lane);
+    gb.load_k(rB, 0, lane);
+    while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
       ga.init(rA, tm * BM, M, warp, lane);
       gb.init(cB, tn * BN, N, warp, lane);
-      for (int kt = 0; kt < KT; ++kt, ++it) {
+      if (kpre != kb) {
+        ga.load_k(cA, kb * BK, lane);
+        gb.load_k(rB, kb * BK, lane);
+      }
+      for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
-        ga.load_k(cA, kt * BK, lane);
-        gb.load_k(rB, kt * BK, lane);
         float* st = stage0 + s * kStage;
         ga.issue(st, A, kt * BK, K, warp, lane);
         gb.issue(st + 2 * kTile, B, kt * BK, K, warp, lane);
         mbar_cp_async_arrive(&full[s]);
+        kpre = kt + 1 < ke ? kt + 1 : 0;
+        ga.load_k(cA, kpre * BK, lane);
+        gb.load_k(rB, kpre * BK, lane);
       }
     }
     cp_async_wait_all();
-  } else if (warp < 8) {
+  } else if (warp < kEpi0) {
     // ---------------------------------- converters ---------------------------------
-    const int t = threadIdx.x - 128;
+    const int t = threadIdx.x - kConv0 * 32;
     uint32_t it = 0;
-    for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
-      for (int kt = 0; kt < KT; ++kt, ++it) {
+    while (wi.next(tile, kb, ke, sk)) {
+      for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
         mbar_wait(&full[s], (it / STAGES) & 1);
         float* st = stage0 + s * kStage;
@@ -224,8 +275,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           for (int i = t; i < kTile / 4; i += 128) {
             const float4 x = hi[i];
             float4 h;
+#if TC_UMMA_HI_TRUNC
+            // hi stays the raw fp32 value: the tensor core reads only its tf32 bits (truncation),
+            // so hi = trunc(x) and only lo = x - trunc(x) is written
+            h.x = tf32_trunc(x.x); h.y = tf32_trunc(x.y); h.z = tf32_trunc(x.z); h.w = tf32_trunc(x.w);
+#else
             h.x = tf32_rna(x.x); h.y = tf32_rna(x.y); h.z = tf32_rna(x.z); h.w = tf32_rna(x.w);
             hi[i] = h;
+#endif
             // lo rounded to tf32 as well: the tensor core would otherwise truncate its low
             // mantissa bits, a bias that grows with K
             lo[i] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
@@ -233,40 +290,46 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           }
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the MMA
-#ifdef TC_UMMA_DEBUG
-        if (blockIdx.x == 0 && it == 0 && t == 0) {
-          printf("A_MN=%d B_MN=%d K=%d M=%d N=%d\n", (int)A_MN, (int)B_MN, K, M, N);
-          for (int i = 0; i < 8; ++i)
-            printf(" Ahi[%d]=%f Alo=%g Bhi[%d]=%f Blo=%g\n", i, st[i], st[kTile + i], i,
-                   st[2 * kTile + i], st[3 * kTile + i]);
-          printf(" A(r=1,k=0)=%f A(r=0,k=1)=%f B(r=1,k=0)=%f B(r=0,k=1)=%f\n",
-                 st[tile_off<A_MN>(1, 0)], st[tile_off<A_MN>(0, 1)],
-                 st[2 * kTile + tile_off<B_MN>(1, 0)], st[2 * kTile + tile_off<B_MN>(0, 1)]);
-        }
-#endif
         mbar_arrive(&conv[s]);
       }
     }
-  } else if (warp < 12) {
+  } else if (warp < kMmaW) {
     // ---------------------------------- epilogue -----------------------------------
-    // TMEM columns: chunk accumulators at 0 and 128 (alternating), the tile's running sum at 256
-    const int q = warp - 8;                 // TMEM lane quarter of this warp
+    // TMEM columns: chunk accumulators at 0 and 128 (alternating), the item's running sum at 256
+    const int q = warp - kEpi0;                // TMEM lane quarter of this warp
     const int row = 32 * q + lane;
     const uint32_t lanes = (uint32_t)(32 * q) << 16;
-    const int nchunks = (KT + kChunkSteps - 1) / kChunkSteps;
     uint32_t ch = 0;
-    for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
       const int m = tm * BM + row;
       const bool min_ = m < M;
       const IDX rc = min_ ? rC[m] : 0;
       const int n0 = tn * BN;
+      const int nchunks = (ke - kb + kChunkSteps - 1) / kChunkSteps;
+      // stream-K piece order (sched.cuh): piece 0 writes alpha*acc + beta*C, piece j >= 1
+      // waits for flag == j and adds alpha*acc; a piece that is not the last publishes j + 1
+      const bool split = sk && !(kb == 0 && ke == sched.KT);
+      int piece = 0;
+      int* flag = nullptr;
+      if (split) {
+        const int s_local = tile - sched.D;
+        const long long g_first = (long long)s_local * sched.KT;
+        const int owner = (int)(((g_first + 1) * sched.P_sk + sched.I - 1) / sched.I) - 1;
+        piece = blockIdx.x - owner;
+        flag = flags + s_local;
+      }
       for (int c = 0; c < nchunks; ++c, ++ch) {
         const int cb = ch & 1;
+        const bool last = c == nchunks - 1;
+        if (last && piece > 0) {
+          if (threadIdx.x == kEpi0 * 32)
+            while (ld_acquire(flag) != piece) __nanosleep(64);
+          epi_sync();
+        }
         mbar_wait(&tfull[cb], (ch >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const bool last = c == nchunks - 1;
 #pragma unroll 1
         for (int c0 = 0; c0 < 4; ++c0) {
           uint32_t u[32];
@@ -290,7 +353,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               if (n < N) {
                 float* p = C + (rc + __ldg(cC + n));
                 double out = alpha * static_cast<double>(__uint_as_float(u[i]));
-                if (beta != 0.0) out = fma(beta, static_cast<double>(*p), out);
+                if (piece > 0) out += static_cast<double>(*p);
+                else if (beta != 0.0) out = fma(beta, static_cast<double>(*p), out);
                 *p = static_cast<float>(out);
               }
             }
@@ -300,17 +364,27 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         mbar_arrive(&tempty[cb]);           // chunk accumulator cb may be overwritten now
       }
+      if (split) {
+        // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
+        // again when the kernel ends (no per-launch reset)
+        epi_sync();
+        if (threadIdx.x == kEpi0 * 32) {
+          __threadfence();
+          st_release(flag, ke < sched.KT ? piece + 1 : 0);
+        }
+      }
     }
   } else {
     // ---------------------------------- MMA issuer ---------------------------------
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                           ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
     uint32_t it = 0, ch = 0;
-    for (int tile = blockIdx.x; tile < T; tile += gridDim.x) {
+    while (wi.next(tile, kb, ke, sk)) {
       uint32_t d = 0;
-      for (int kt = 0; kt < KT; ++kt, ++it) {
-        const bool chunk_start = kt % kChunkSteps == 0;
+      for (int kt = kb; kt < ke; ++kt, ++it) {
+        const int j0 = (kt - kb) % kChunkSteps;
+        const bool chunk_start = j0 == 0;
+        const bool chunk_end = j0 == kChunkSteps - 1 || kt == ke - 1;
         if (chunk_start) {
           const int cb = ch & 1;
           if (ch >= 2) mbar_wait(&tempty[cb], ((ch >> 1) - 1) & 1);
@@ -329,32 +403,31 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
           for (int j = 0; j < BK / 8; ++j) {
             const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-            mma_tf32(d, make_desc<A_MN>(ah, j), make_desc<B_MN>(bh, j), idesc, acc0);
-            mma_tf32(d, make_desc<A_MN>(ah, j), make_desc<B_MN>(bl, j), idesc, 1u);
-            mma_tf32(d, make_desc<A_MN>(al, j), make_desc<B_MN>(bh, j), idesc, 1u);
+            mma_tf32(d, make_desc(ah, j), make_desc(bh, j), idesc, acc0);
+            mma_tf32(d, make_desc(ah, j), make_desc(bl, j), idesc, 1u);
+            mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
           }
           mma_commit(&empty[s]);                       // stage s is free once these complete
-          if (kt % kChunkSteps == kChunkSteps - 1 || kt == KT - 1)
-            mma_commit(&tfull[ch & 1]);                // this chunk's accumulator is complete
+          if (chunk_end) mma_commit(&tfull[ch & 1]);   // this chunk's accumulator is complete
         }
         __syncwarp();
-        if (kt % kChunkSteps == kChunkSteps - 1 || kt == KT - 1) ++ch;
+        if (chunk_end) ++ch;
       }
     }
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (warp == 12) {
+  if (warp == kMmaW) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tmem));
   }
 }
 
-template <typename IDX, bool A_MN, bool B_MN>
+template <typename IDX, bool A_KR, bool B_KR>
 static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   constexpr int smem = STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 4) * 8 + 16;
-  auto kern = tc_umma_f32_kernel<IDX, A_MN, B_MN>;
+  auto kern = tc_umma_f32_kernel<IDX, A_KR, B_KR>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -362,27 +435,39 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int KT = (a.K + BK - 1) / BK;
   const int T = tiles_m * tiles_n;
-  const int grid = T < a.num_sms ? T : a.num_sms;
+  // stream-K only when the partial wave is < 70% full: split pieces cost this kernel more than
+  // the DMMA one (cfg4 fp32: a 74-86% partial wave ran 8-13% faster whole, a < 30% one 10-20%
+  // faster split; profiles/r01/ab_umma_sk.txt). TC_UMMA_SK=0 turns the tail off.
+  const char* pe = getenv("TC_UMMA_SK");
+  const bool sk = a.stream_k && !(pe && !strcmp(pe, "0"));
+  Sched sc = make_sched(T, KT, a.num_sms, sk, 70);
+  if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, a.num_sms, false);
+  sc.wave_sync = 0;
+  const int grid = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
   kern<<<grid, kThreads, smem, s>>>(
       static_cast<const float*>(a.A), static_cast<const float*>(a.B), static_cast<float*>(a.C),
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
       static_cast<const IDX*>(a.rB), static_cast<const IDX*>(a.cB),
       static_cast<const IDX*>(a.rC), static_cast<const IDX*>(a.cC), a.M, a.N, a.K, tiles_m,
-      tiles_n, a.alpha, a.beta);
+      tiles_n, a.alpha, a.beta, sc, a.flags);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 }  // namespace umma
 
 // fp32 through the tensor cores (3xTF32). Applies to int32-offset fp32 contractions with
-// K >= 1. Both operands are staged K-major: the MN-major (transposed) tf32 operand mode left
-// the accumulator at zero on this part (tools/calib/umma_tf32_test.cu sweeps it), and the
-// core-matrix lane mapping reads full 32-byte sectors from an M-contiguous operand anyway.
+// K >= 1. The gather lane mapping of each operand follows its leading direction (plan.cpp:
+// A is read along M when a_vec_m, B along K when b_vec_k).
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_umma_f32(const LaunchArgs& a, cudaStream_t stream) {
   if (!a.f32 || a.idx64 || a.K < 1) return 0;
-  return umma::launch_dir<int, false, false>(a, stream);
+  const bool akr = !a.a_vec_m, bkr = a.b_vec_k;
+  if (akr) return bkr ? umma::launch_dir<int, true, true>(a, stream)
+                      : umma::launch_dir<int, true, false>(a, stream);
+  return bkr ? umma::launch_dir<int, false, true>(a, stream)
+             : umma::launch_dir<int, false, false>(a, stream);
 }
 
 }  // namespace tcb

@@ -470,6 +470,36 @@ def test_stream_k_splits(mnk, beta):
     check(case, bitwise=True)
 
 
+@pytest.mark.usefixtures("both_f32_paths")
+@pytest.mark.parametrize("mnk", [(100, 120, 20000), (1000, 1200, 700), (128 * 12, 128 * 13, 2000),
+                                 (2366, 1012, 1935)])
+@pytest.mark.parametrize("beta", [0.0, 0.75])
+def test_stream_k_splits_f32(mnk, beta):
+    """The fp32 kernels' stream-K pieces (fix-up order, beta on the first piece); integer-valued
+    inputs make every partial sum exact, so the split result must match bit for bit."""
+    case = W.Case("skf", "mn", "mk", "kn", dict(zip("mnk", mnk)), alpha=0.5, beta=beta,
+                  c_init="dist", seed=33, dtype=torch.float32)
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
+@pytest.mark.usefixtures("both_f32_paths")
+def test_stream_k_deterministic_f32():
+    case = W.Case("skdf", "mn", "mk", "kn", {"m": 2366, "n": 1012, "k": 1935}, alpha=1.0,
+                  beta=0.5, c_init="dist", seed=34, dtype=torch.float32)
+    Ad, Bd, Cd = W.make_tensors(case, "cuda")
+    outs = []
+    for _ in range(3):
+        C = Cd.clone()
+        tc().contract(case.spec, Ad, Bd, C, case.alpha, case.beta)
+        outs.append(C)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    ref = case.alpha * (Ad.double() @ Bd.double()) + case.beta * Cd.double()
+    assert relerr(outs[0].cpu().numpy(), ref.cpu().numpy()) < 1e-5
+
+
 def test_stream_k_deterministic_and_matches_data_parallel():
     case = W.Case("skd", "mn", "mk", "kn", {"m": 1900, "n": 1700, "k": 3000}, alpha=1.0,
                   beta=0.5, c_init="dist", seed=32)

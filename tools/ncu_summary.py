@@ -52,6 +52,22 @@ def main(path):
                         stalls.append((float(v.replace(",", "")), k[34:-23]))
                     except ValueError:
                         pass
+            # the busiest units: every *.pct_of_peak_sustained_* throughput metric, top 20
+            pk = []
+            for k, v in d.items():
+                if "pct_of_peak_sustained" in k and ("throughput" in k or "utilization" in k
+                                                     or "_cycles_active" in k):
+                    try:
+                        pk.append((float(v.replace(",", "")), k))
+                    except ValueError:
+                        pass
+            out.append("  busiest units (% of peak):")
+            for v, k in sorted(pk, reverse=True)[:20]:
+                out.append(f"    {k:86s} {v:7.2f}")
+            for k, v in d.items():
+                if k.startswith("l1tex__") and (k.endswith(".sum") and ("wavefronts" in k or
+                                                "requests" in k or "sectors" in k)):
+                    out.append(f"  {k:86s} {v:>16s}")
             tot = sum(s for s, _ in stalls) or 1.0
             out.append("  warp stalls (per issued instruction; share):")
             for s, name in sorted(stalls, reverse=True)[:10]:
