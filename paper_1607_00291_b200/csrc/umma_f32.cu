@@ -20,9 +20,10 @@
 //               32 (w - 8)..), added into the running sum in TMEM; at the end of a work item
 //               one row of C per thread, alpha * acc + beta * C through rscat_C / cscat_C
 //   warp 12     MMA issuer: one lane issues 3 x 4 tcgen05.mma (M = N = 128, K = 8) per K step and
-//               commits them to the stage's `empty` barrier; two TMEM chunk accumulators let
+//               commits them to the stage's `empty` barrier; three TMEM chunk accumulators let
 //               the epilogue's adds overlap the next chunk's MMAs.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -58,6 +59,11 @@ constexpr int GROUP_M = 2;
 #define TC_UMMA_CHUNK 1
 #endif
 constexpr int kChunkSteps = TC_UMMA_CHUNK;   // K steps of BK per chunk
+// TMEM (512 columns): kChunkBufs chunk accumulators of BN columns, then the running sum; three
+// buffers give the epilogue two chunks of slack while it stores a finished tile
+constexpr int kChunkBufs = 3;
+constexpr int kSumCol = kChunkBufs * BN;
+static_assert(kSumCol + BN <= 512, "TMEM columns");
 
 __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u32(p); }
 
@@ -192,9 +198,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * kStage * sizeof(float));
   uint64_t* conv = full + STAGES;
   uint64_t* empty = conv + STAGES;
-  uint64_t* tfull = empty + STAGES;    // [2]
-  uint64_t* tempty = tfull + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + STAGES;    // [kChunkBufs]
+  uint64_t* tempty = tfull + kChunkBufs;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kChunkBufs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -203,7 +209,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
       mbar_init(&conv[s], 128);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kChunkBufs; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
@@ -295,7 +301,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     }
   } else if (warp < kMmaW) {
     // ---------------------------------- epilogue -----------------------------------
-    // TMEM columns: chunk accumulators at 0 and 128 (alternating), the item's running sum at 256
+    // TMEM columns: chunk accumulators at 0, 128, 256 (round robin), the item's running sum at 384
     const int q = warp - kEpi0;                // TMEM lane quarter of this warp
     const int row = 32 * q + lane;
     const uint32_t lanes = (uint32_t)(32 * q) << 16;
@@ -320,15 +326,26 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         piece = blockIdx.x - owner;
         flag = flags + s_local;
       }
+      const bool read_c = piece > 0 || beta != 0.0;
+#ifdef TC_UMMA_TRACE
+      unsigned long long tr0, tr1 = 0, tr2 = 0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+#endif
       for (int c = 0; c < nchunks; ++c, ++ch) {
-        const int cb = ch & 1;
+        const int cb = ch % kChunkBufs;
         const bool last = c == nchunks - 1;
         if (last && piece > 0) {
+#ifdef TC_UMMA_TRACE
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+#endif
           if (threadIdx.x == kEpi0 * 32)
             while (ld_acquire(flag) != piece) __nanosleep(64);
           epi_sync();
+#ifdef TC_UMMA_TRACE
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
+#endif
         }
-        mbar_wait(&tfull[cb], (ch >> 1) & 1);
+        mbar_wait(&tfull[cb], (ch / kChunkBufs) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
         for (int c0 = 0; c0 < 4; ++c0) {
@@ -336,7 +353,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           tmem_ld32(tmem + lanes + (uint32_t)(cb * BN + 32 * c0), u);
           if (c > 0) {
             uint32_t t2[32];
-            tmem_ld32(tmem + lanes + (uint32_t)(2 * BN + 32 * c0), t2);
+            tmem_ld32(tmem + lanes + (uint32_t)(kSumCol + 32 * c0), t2);
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -345,17 +362,36 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
           }
           if (!last) {
-            tmem_st32(tmem + lanes + (uint32_t)(2 * BN + 32 * c0), u);
-          } else if (min_) {
+            tmem_st32(tmem + lanes + (uint32_t)(kSumCol + 32 * c0), u);
+          } else {
+            // final values of 32 columns: the column offsets (one coalesced load, shuffled
+            // out), then all reads of C, then all stores, so the memory round trips overlap
+            // instead of one dependent read per element
+            const int nb = n0 + 32 * c0;
+            const bool full = nb + 32 <= N;
+            const IDX col = (full || nb + lane < N) ? __ldg(cC + nb + lane) : 0;
+            // (no branch on the row: the shuffles need the whole warp)
+            if (read_c) {
+              float old[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int n = n0 + 32 * c0 + i;
-              if (n < N) {
-                float* p = C + (rc + __ldg(cC + n));
+              for (int i = 0; i < 32; ++i) {
+                const IDX o = __shfl_sync(0xffffffffu, col, i);
+                old[i] = (min_ && (full || nb + i < N)) ? C[rc + o] : 0.f;
+              }
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const IDX o = __shfl_sync(0xffffffffu, col, i);
                 double out = alpha * static_cast<double>(__uint_as_float(u[i]));
-                if (piece > 0) out += static_cast<double>(*p);
-                else if (beta != 0.0) out = fma(beta, static_cast<double>(*p), out);
-                *p = static_cast<float>(out);
+                out = piece > 0 ? out + static_cast<double>(old[i])
+                                : fma(beta, static_cast<double>(old[i]), out);
+                if (min_ && (full || nb + i < N)) C[rc + o] = static_cast<float>(out);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const IDX o = __shfl_sync(0xffffffffu, col, i);
+                if (min_ && (full || nb + i < N))
+                  C[rc + o] = static_cast<float>(alpha * static_cast<double>(__uint_as_float(u[i])));
               }
             }
           }
@@ -373,6 +409,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           st_release(flag, ke < sched.KT ? piece + 1 : 0);
         }
       }
+#ifdef TC_UMMA_TRACE
+      if (threadIdx.x == kEpi0 * 32) {
+        unsigned long long tr3;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr3));
+        printf("TR cta %d tile %d kb %d ke %d piece %d start %llu wait0 %llu wait1 %llu end %llu\n",
+               (int)blockIdx.x, tile, kb, ke, piece, tr0, tr1, tr2, tr3);
+      }
+#endif
     }
   } else {
     // ---------------------------------- MMA issuer ---------------------------------
@@ -386,8 +430,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         const bool chunk_start = j0 == 0;
         const bool chunk_end = j0 == kChunkSteps - 1 || kt == ke - 1;
         if (chunk_start) {
-          const int cb = ch & 1;
-          if (ch >= 2) mbar_wait(&tempty[cb], ((ch >> 1) - 1) & 1);
+          const int cb = ch % kChunkBufs;
+          if (ch >= kChunkBufs) mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           d = tmem + (uint32_t)(cb * BN);
         }
@@ -408,7 +452,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
           }
           mma_commit(&empty[s]);                       // stage s is free once these complete
-          if (chunk_end) mma_commit(&tfull[ch & 1]);   // this chunk's accumulator is complete
+          if (chunk_end) mma_commit(&tfull[ch % kChunkBufs]);   // this chunk's accumulator is complete
         }
         __syncwarp();
         if (chunk_end) ++ch;
@@ -426,7 +470,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 
 template <typename IDX, bool A_KR, bool B_KR>
 static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
-  constexpr int smem = STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 4) * 8 + 16;
+  constexpr int smem = STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs) * 8 + 16;
   auto kern = tc_umma_f32_kernel<IDX, A_KR, B_KR>;
   static bool attr = false;
   if (!attr) {
