@@ -306,6 +306,10 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     const int row = 32 * q + lane;
     const uint32_t lanes = (uint32_t)(32 * q) << 16;
     uint32_t ch = 0;
+#ifdef TC_UMMA_TRACE
+    int ntr = 0, trm[4][4];
+    unsigned long long trt[4][4];
+#endif
     while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
@@ -410,14 +414,22 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         }
       }
 #ifdef TC_UMMA_TRACE
-      if (threadIdx.x == kEpi0 * 32) {
+      if (ntr < 4) {
         unsigned long long tr3;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr3));
-        printf("TR cta %d tile %d kb %d ke %d piece %d start %llu wait0 %llu wait1 %llu end %llu\n",
-               (int)blockIdx.x, tile, kb, ke, piece, tr0, tr1, tr2, tr3);
+        trm[ntr][0] = tile; trm[ntr][1] = kb; trm[ntr][2] = ke; trm[ntr][3] = piece;
+        trt[ntr][0] = tr0; trt[ntr][1] = tr1; trt[ntr][2] = tr2; trt[ntr][3] = tr3;
+        ++ntr;
       }
 #endif
     }
+#ifdef TC_UMMA_TRACE
+    if (threadIdx.x == kEpi0 * 32)
+      for (int i = 0; i < ntr; ++i)
+        printf("TR cta %d tile %d kb %d ke %d piece %d start %llu wait0 %llu wait1 %llu end %llu\n",
+               (int)blockIdx.x, trm[i][0], trm[i][1], trm[i][2], trm[i][3], trt[i][0], trt[i][1],
+               trt[i][2], trt[i][3]);
+#endif
   } else {
     // ---------------------------------- MMA issuer ---------------------------------
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |

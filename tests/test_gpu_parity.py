@@ -485,6 +485,21 @@ def test_stream_k_splits_f32(mnk, beta):
 
 
 @pytest.mark.usefixtures("both_f32_paths")
+@pytest.mark.parametrize("k", [1024, 16384])
+def test_f32_one_signed_bias(k):
+    """One-signed data (U[0, 1)) lets accumulation biases add up instead of cancelling; the
+    tcgen05 kernel's chunked accumulation (R18) keeps the error K-independent, measured
+    7.6e-7 (profiles/r01/ab_umma_chunk.txt). Bound: the 1e-5 tolerance with a 5x margin."""
+    g = torch.Generator(device="cuda").manual_seed(k)
+    A = torch.rand(256, k, device="cuda", generator=g)
+    B = torch.rand(k, 192, device="cuda", generator=g)
+    C = torch.empty(256, 192, device="cuda")
+    tc().contract("mn-mk-kn", A, B, C)
+    ref = A.double() @ B.double()
+    assert ((C.double() - ref).norm() / ref.norm()).item() < 2e-6
+
+
+@pytest.mark.usefixtures("both_f32_paths")
 def test_stream_k_deterministic_f32():
     case = W.Case("skdf", "mn", "mk", "kn", {"m": 2366, "n": 1012, "k": 1935}, alpha=1.0,
                   beta=0.5, c_init="dist", seed=34, dtype=torch.float32)
