@@ -39,7 +39,15 @@ namespace umma {
 using namespace dev;
 using namespace sched;
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3;
+// A operand in tensor memory (TC_UMMA_TMEM_A=1): the converter warps write A's hi and lo to TMEM
+// with tcgen05.st (lane = row of A, one column per k) and the MMAs take A from there, so A's lo
+// never goes to shared memory and the tensor core reads only B from it; the freed shared memory
+// buys a fourth stage. Off: A hi and lo are staged in shared memory like B.
+#ifndef TC_UMMA_TMEM_A
+#define TC_UMMA_TMEM_A 1
+#endif
+constexpr bool kTmemA = TC_UMMA_TMEM_A;
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = kTmemA ? 4 : 3;
 #ifndef TC_UMMA_PW
 #define TC_UMMA_PW 4
 #endif
@@ -47,7 +55,9 @@ constexpr int kPW = TC_UMMA_PW;            // producer warps (4 or 8)
 constexpr int kConv0 = kPW, kEpi0 = kPW + 4, kMmaW = kPW + 8;   // first warp of each role
 constexpr int kThreads = (kPW + 9) * 32;
 constexpr int kTile = (BK / 4) * (128 * 4 + 16);   // floats per operand tile (padded K chunks)
-constexpr int kStage = 4 * kTile;        // A hi, A lo, B hi, B lo
+// stage layout: [A hi (raw), A lo, B hi (raw), B lo], or [A raw, B hi (raw), B lo] with A in TMEM
+constexpr int kStage = (kTmemA ? 3 : 4) * kTile;
+constexpr int kOffAl = kTile, kOffBh = kTmemA ? kTile : 2 * kTile, kOffBl = kOffBh + kTile;
 constexpr int GROUP_M = 2;
 // The tensor core's fp32 accumulation is biased (it truncates): on one-signed data the relative
 // error grows with the number of MMAs chained into one accumulator (3xTF32, K = 128 per
@@ -61,9 +71,11 @@ constexpr int GROUP_M = 2;
 constexpr int kChunkSteps = TC_UMMA_CHUNK;   // K steps of BK per chunk
 // TMEM (512 columns): kChunkBufs chunk accumulators of BN columns, then the running sum; three
 // buffers give the epilogue two chunks of slack while it stores a finished tile
-constexpr int kChunkBufs = 3;
+// (two with A in TMEM, whose two 64-column slots -- hi, lo -- take the last 128 columns)
+constexpr int kChunkBufs = kTmemA ? 2 : 3;
 constexpr int kSumCol = kChunkBufs * BN;
-static_assert(kSumCol + BN <= 512, "TMEM columns");
+constexpr int kACol = kSumCol + BN, kASlots = 2;
+static_assert(kSumCol + BN + (kTmemA ? kASlots * 2 * BK : 0) <= 512, "TMEM columns");
 
 __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u32(p); }
 
@@ -92,6 +104,12 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
   asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
                :: "r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                            uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+               " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+               :: "r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
@@ -200,7 +218,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   uint64_t* empty = conv + STAGES;
   uint64_t* tfull = empty + STAGES;    // [kChunkBufs]
   uint64_t* tempty = tfull + kChunkBufs;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kChunkBufs);
+  uint64_t* aempty = tempty + kChunkBufs;   // [kASlots] (A in TMEM)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kASlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -213,6 +232,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    for (int a = 0; a < kASlots; ++a) mbar_init(&aempty[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == kMmaW) {
@@ -256,7 +276,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
         float* st = stage0 + s * kStage;
         ga.issue(st, A, kt * BK, K, warp, lane);
-        gb.issue(st + 2 * kTile, B, kt * BK, K, warp, lane);
+        gb.issue(st + kOffBh, B, kt * BK, K, warp, lane);
         mbar_cp_async_arrive(&full[s]);
         kpre = kt + 1 < ke ? kt + 1 : 0;
         ga.load_k(cA, kpre * BK, lane);
@@ -274,9 +294,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         mbar_wait(&full[s], (it / STAGES) & 1);
         float* st = stage0 + s * kStage;
 #pragma unroll
-        for (int op = 0; op < 2; ++op) {          // A, then B: hi buffer, lo buffer after it
-          float4* hi = reinterpret_cast<float4*>(st + op * 2 * kTile);
-          float4* lo = reinterpret_cast<float4*>(st + op * 2 * kTile + kTile);
+        for (int op = kTmemA ? 1 : 0; op < 2; ++op) {   // A (in smem), then B: hi, lo buffers
+          float4* hi = reinterpret_cast<float4*>(st + (op ? kOffBh : 0));
+          float4* lo = reinterpret_cast<float4*>(st + (op ? kOffBl : kOffAl));
 #pragma unroll
           for (int i = t; i < kTile / 4; i += 128) {
             const float4 x = hi[i];
@@ -294,6 +314,31 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             lo[i] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
                                 tf32_rna(x.w - h.w));
           }
+        }
+        if constexpr (kTmemA) {
+          // A to tensor memory: this thread's row (TMEM lane 32 q + lane), 32 K values
+          const int q = warp - kConv0;
+          const int row = 32 * q + lane;
+          const uint32_t slot = it % kASlots;
+          if (it >= kASlots) mbar_wait(&aempty[slot], ((it / kASlots) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          uint32_t h[32], lo[32];
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            const float4 x = *reinterpret_cast<const float4*>(st + tile_off(row, 4 * c));
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float hv = tf32_trunc(xs[e]);
+              h[4 * c + e] = __float_as_uint(hv);
+              lo[4 * c + e] = __float_as_uint(tf32_rna(xs[e] - hv));
+            }
+          }
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + slot * 2 * BK);
+          tmem_st32(ta, h);
+          tmem_st32(ta + BK, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the MMA
         mbar_arrive(&conv[s]);
@@ -452,16 +497,29 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
           const float* st = stage0 + s * kStage;
-          const float* ah = st;
-          const float* al = st + kTile;
-          const float* bh = st + 2 * kTile;
-          const float* bl = st + 3 * kTile;
+          const float* bh = st + kOffBh;
+          const float* bl = st + kOffBl;
+          if constexpr (kTmemA) {
+            const uint32_t slot = it % kASlots;
+            const uint32_t ah = tmem + (uint32_t)(kACol + slot * 2 * BK), al = ah + BK;
 #pragma unroll
-          for (int j = 0; j < BK / 8; ++j) {
-            const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-            mma_tf32(d, make_desc(ah, j), make_desc(bh, j), idesc, acc0);
-            mma_tf32(d, make_desc(ah, j), make_desc(bl, j), idesc, 1u);
-            mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
+            for (int j = 0; j < BK / 8; ++j) {
+              const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
+              mma_tf32_ta(d, ah + 8 * j, make_desc(bh, j), idesc, acc0);
+              mma_tf32_ta(d, ah + 8 * j, make_desc(bl, j), idesc, 1u);
+              mma_tf32_ta(d, al + 8 * j, make_desc(bh, j), idesc, 1u);
+            }
+            mma_commit(&aempty[slot]);                 // A slot free once these complete
+          } else {
+            const float* ah = st;
+            const float* al = st + kOffAl;
+#pragma unroll
+            for (int j = 0; j < BK / 8; ++j) {
+              const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
+              mma_tf32(d, make_desc(ah, j), make_desc(bh, j), idesc, acc0);
+              mma_tf32(d, make_desc(ah, j), make_desc(bl, j), idesc, 1u);
+              mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
+            }
           }
           mma_commit(&empty[s]);                       // stage s is free once these complete
           if (chunk_end) mma_commit(&tfull[ch % kChunkBufs]);   // this chunk's accumulator is complete
@@ -482,7 +540,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 
 template <typename IDX, bool A_KR, bool B_KR>
 static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
-  constexpr int smem = STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs) * 8 + 16;
+  constexpr int smem =
+      STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs + kASlots) * 8 + 16;
   auto kern = tc_umma_f32_kernel<IDX, A_KR, B_KR>;
   static bool attr = false;
   if (!attr) {
