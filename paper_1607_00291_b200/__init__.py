@@ -158,19 +158,50 @@ def tc_contract_host(dtype: int, alpha: float, A: Desc, B: Desc, beta: float, C:
 
 
 _specs = {}
+torch_C = None   # torch._C, bound on the first contract() call (the import stays torch-free)
 
 
 def contract(spec: str, A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
     """C := alpha * A.B + beta * C for torch CUDA tensors, asynchronously on `stream`
-    (default: the current torch stream). Returns C."""
-    labels = _specs.get(spec)
-    if labels is None:
-        labels = _specs[spec] = parse_spec(spec)
-    lc, la, lb = labels
+    (default: the current torch stream). Returns C.
+
+    The descriptors of a (spec, dtype, shapes, strides) combination are built once per thread;
+    a repeated call only refreshes the three data pointers before the C-ABI call (the library
+    then finds its cached plan), which keeps the host cost of small contractions low."""
+    fast = getattr(_tls, "fast", None)
+    if fast is None:
+        fast = _tls.fast = {}
+    key = (spec, C.dtype, A.shape, A.stride(), B.shape, B.stride(), C.shape, C.stride())
+    ent = fast.get(key)
+    if ent is None:
+        global torch_C
+        if torch_C is None:
+            import torch
+            torch_C = torch._C
+        labels = _specs.get(spec)
+        if labels is None:
+            labels = _specs[spec] = parse_spec(spec)
+        lc, la, lb = labels
+        dA = Desc(la, list(A.shape), list(A.stride()), 0)
+        dB = Desc(lb, list(B.shape), list(B.stride()), 0)
+        dC = Desc(lc, list(C.shape), list(C.stride()), 0)
+        if len(fast) > 256:
+            fast.clear()
+        ent = fast[key] = (_dtype_code(C.dtype), dA.t, dB.t, dC.t, ctypes.byref(dA.t),
+                           ctypes.byref(dB.t), ctypes.byref(dC.t), (dA, dB, dC))
     if not (A.is_cuda and B.is_cuda and C.is_cuda):
         raise ValueError("contract() takes CUDA tensors; use contract_host() for host memory")
-    tc_contract(_dtype_code(C.dtype), alpha, _desc(A, la, 0), _desc(B, lb, 1), beta,
-                _desc(C, lc, 2), _stream_ptr(stream))
+    code, tA, tB, tC, pA, pB, pC, _ = ent
+    tA.data = A.data_ptr()
+    tB.data = B.data_ptr()
+    tC.data = C.data_ptr()
+    if stream is None:
+        sp = torch_C._cuda_getCurrentRawStream(torch_C._cuda_getDevice())
+    else:
+        sp = stream.cuda_stream
+    rc = _lib.tc_contract(code, alpha, pA, pB, beta, pC, sp)
+    if rc != 0:
+        raise TCError(rc)
     return C
 
 

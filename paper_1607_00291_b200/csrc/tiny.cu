@@ -18,36 +18,50 @@ constexpr int kThreads = 128;   // consecutive m (C's unit-stride bundle, P:930-
 constexpr int kNB = 4;          // columns of C per thread (B values shared through smem)
 constexpr int kMaxK = 256;
 
-// CTA = 128 consecutive rows x kNB columns of C. The CTA first stages A's K offsets and its
-// kNB columns of B (K x kNB values) in shared memory, so the K loop issues one independent
-// global load per k (A, coalesced along M when A is) instead of two dependent table lookups
-// and two operand loads; each A value feeds kNB multiply-adds.
+// CTA = 128 consecutive rows x kNB columns of C. The CTA stages its kNB columns of B (K x kNB
+// values) in shared memory; each thread loads A's values for its row kKB at a time into
+// registers (K offsets read straight from the table: every lane reads the same entry, one
+// broadcast), so a K loop of 64 costs two global round trips instead of eight, and the first
+// block of A is already in flight while B is being staged. Each A value feeds kNB
+// multiply-adds.
+constexpr int kKB = 32;
 template <typename T, typename IDX>
 __global__ void __launch_bounds__(kThreads) tc_tiny_kernel(
     const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
     const IDX* __restrict__ rA, const IDX* __restrict__ cA, const IDX* __restrict__ rB,
     const IDX* __restrict__ cB, const IDX* __restrict__ rC, const IDX* __restrict__ cC, int M,
     int N, int K, double alpha, double beta) {
-  __shared__ IDX cas[kMaxK];
   __shared__ double bs[kMaxK][kNB];
   const int m = blockIdx.x * kThreads + threadIdx.x;
   const int n0 = blockIdx.y * kNB;
-  for (int k = threadIdx.x; k < K; k += kThreads) cas[k] = cA[k];
+  const bool mv = m < M;
+  const IDX ra = mv ? rA[m] : 0;
+  double a[kKB];
+#pragma unroll
+  for (int j = 0; j < kKB; ++j)
+    a[j] = (mv && j < K) ? static_cast<double>(A[ra + __ldg(cA + j)]) : 0.0;
   for (int e = threadIdx.x; e < K * kNB; e += kThreads) {
     const int k = e / kNB, j = e - k * kNB;
     bs[k][j] = n0 + j < N ? static_cast<double>(B[rB[k] + cB[n0 + j]]) : 0.0;
   }
   __syncthreads();
-  if (m >= M) return;
-  const IDX ra = rA[m];
+  if (!mv) return;
   double acc[kNB];
 #pragma unroll
   for (int j = 0; j < kNB; ++j) acc[j] = 0.0;
-#pragma unroll 8
-  for (int k = 0; k < K; ++k) {
-    const double a = static_cast<double>(A[ra + cas[k]]);
+  for (int k0 = 0; k0 < K; k0 += kKB) {
+    if (k0 > 0) {
 #pragma unroll
-    for (int j = 0; j < kNB; ++j) acc[j] = fma(a, bs[k][j], acc[j]);
+      for (int j = 0; j < kKB; ++j)
+        a[j] = k0 + j < K ? static_cast<double>(A[ra + __ldg(cA + k0 + j)]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < kKB; ++j) {
+      if (k0 + j < K) {
+#pragma unroll
+        for (int c = 0; c < kNB; ++c) acc[c] = fma(a[j], bs[k0 + j][c], acc[c]);
+      }
+    }
   }
   const IDX rc = rC[m];
 #pragma unroll
