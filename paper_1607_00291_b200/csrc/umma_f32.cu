@@ -199,11 +199,83 @@ struct Gather {
   }
 };
 
+// 16-byte vector gathers (the block-scatter decision of P:644-683 at 4-float granularity), used
+// when the plan proved every vector of the operand contiguous and 16-byte aligned (a_vec_all /
+// b_vec_all): a quarter of the copy instructions of the element gathers.
+//  GatherVK: vectors along K (4 consecutive k of one row) into the K-major staging layout;
+//            lanes = 4 rows x 8 vectors, i.e. 4 full 128-byte runs per instruction
+//  GatherVM: vectors along the rows (A only: 4 consecutive m at one k) into a [k][m] staging
+//            layout (row k = 128 floats) that the converter warps read column-wise into TMEM;
+//            one instruction = one k, 128 consecutive m
+template <typename IDX>
+struct GatherVK {
+  static constexpr int NR = 128 / 4 / kPW;           // row groups of 4 per warp
+  IDX ro[NR];
+  uint32_t rv;
+  IDX ko;
+  __device__ __forceinline__ static int row(int w, int i, int l) { return 4 * (w * NR + i) + (l >> 3); }
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+    rv = 0;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int r = base + row(w, i, l);
+      ro[i] = rtab[r];
+      rv |= (r < extent ? 1u : 0u) << i;
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    ko = __ldg(ktab + k0 + 4 * (l & 7));
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+    const int kk = 4 * (l & 7);
+    const bool kin = k0 + kk < K;                    // K is a multiple of 4 here
+#pragma unroll
+    for (int i = 0; i < NR; ++i)
+      cp_async16(sm + tile_off(row(w, i, l), kk), g + (ro[i] + ko), kin && ((rv >> i) & 1u));
+  }
+};
+
+template <typename IDX>
+struct GatherVM {
+  static constexpr int NKW = BK / kPW;               // k rows per warp
+  IDX ro;
+  bool rv;
+  IDX ko[NKW];
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+    const int r = base + 4 * l;
+    ro = rtab[r];
+    rv = r < extent;                                 // M is a multiple of 4 here
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    const int w = (threadIdx.x >> 5);
+#pragma unroll
+    for (int j = 0; j < NKW; ++j) ko[j] = __ldg(ktab + k0 + w * NKW + j);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int j = 0; j < NKW; ++j) {
+      const int k = w * NKW + j;
+      cp_async16(sm + k * BM + 4 * l, g + (ro + ko[j]), rv && k0 + k < K);
+    }
+  }
+};
+
+// operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors
+template <typename IDX, int MODE> struct GatherSel;
+template <typename IDX> struct GatherSel<IDX, 0> { using type = Gather<IDX, false>; };
+template <typename IDX> struct GatherSel<IDX, 1> { using type = Gather<IDX, true>; };
+template <typename IDX> struct GatherSel<IDX, 2> { using type = GatherVK<IDX>; };
+template <typename IDX> struct GatherSel<IDX, 3> { using type = GatherVM<IDX>; };
+
 __device__ __forceinline__ void epi_sync() {   // the four epilogue warps only
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
 }
 
-template <typename IDX, bool A_KR, bool B_KR>
+template <typename IDX, int A_MODE, int B_MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, float* __restrict__ C,
                    const IDX* __restrict__ rA, const IDX* __restrict__ cA,
@@ -254,8 +326,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 
   if (warp < kPW) {
     // ---------------------------------- producers ----------------------------------
-    Gather<IDX, A_KR> ga;
-    Gather<IDX, B_KR> gb;
+    typename GatherSel<IDX, A_MODE>::type ga;
+    typename GatherSel<IDX, B_MODE>::type gb;
     uint32_t it = 0;
     // K offsets depend on the K step only: those of the next step are fetched while this one's
     // copies are in flight, so the table reads stay off the producer's critical path
@@ -325,7 +397,13 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           uint32_t h[32], lo[32];
 #pragma unroll
           for (int c = 0; c < BK / 4; ++c) {
-            const float4 x = *reinterpret_cast<const float4*>(st + tile_off(row, 4 * c));
+            float4 x;
+            if constexpr (A_MODE == 3) {   // [k][m] staging
+              x = make_float4(st[(4 * c) * BM + row], st[(4 * c + 1) * BM + row],
+                              st[(4 * c + 2) * BM + row], st[(4 * c + 3) * BM + row]);
+            } else {
+              x = *reinterpret_cast<const float4*>(st + tile_off(row, 4 * c));
+            }
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -538,11 +616,11 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   }
 }
 
-template <typename IDX, bool A_KR, bool B_KR>
+template <typename IDX, int A_MODE, int B_MODE>
 static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   constexpr int smem =
       STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs + kASlots) * 8 + 16;
-  auto kern = tc_umma_f32_kernel<IDX, A_KR, B_KR>;
+  auto kern = tc_umma_f32_kernel<IDX, A_MODE, B_MODE>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -573,16 +651,30 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
 }  // namespace umma
 
 // fp32 through the tensor cores (3xTF32). Applies to int32-offset fp32 contractions with
-// K >= 1. The gather lane mapping of each operand follows its leading direction (plan.cpp:
-// A is read along M when a_vec_m, B along K when b_vec_k).
+// K >= 1. The gather of each operand follows its leading direction (plan.cpp: A is read along M
+// when a_vec_m, B along K when b_vec_k) and uses 16-byte vectors when the plan proved them all
+// contiguous and aligned (a_vec_all / b_vec_all); an N-contiguous B is always element-gathered
+// (its vectors would not be contiguous in the K-major MMA layout).
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_umma_f32(const LaunchArgs& a, cudaStream_t stream) {
   if (!a.f32 || a.idx64 || a.K < 1) return 0;
-  const bool akr = !a.a_vec_m, bkr = a.b_vec_k;
-  if (akr) return bkr ? umma::launch_dir<int, true, true>(a, stream)
-                      : umma::launch_dir<int, true, false>(a, stream);
-  return bkr ? umma::launch_dir<int, false, true>(a, stream)
-             : umma::launch_dir<int, false, false>(a, stream);
+  const int am = a.a_vec_m ? (a.a_vec_all ? 3 : 0) : (a.a_vec_all ? 2 : 1);
+  const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : 1) : 0;
+  using namespace umma;
+  switch (am * 3 + bm) {
+    case 0: return launch_dir<int, 0, 0>(a, stream);
+    case 1: return launch_dir<int, 0, 1>(a, stream);
+    case 2: return launch_dir<int, 0, 2>(a, stream);
+    case 3: return launch_dir<int, 1, 0>(a, stream);
+    case 4: return launch_dir<int, 1, 1>(a, stream);
+    case 5: return launch_dir<int, 1, 2>(a, stream);
+    case 6: return launch_dir<int, 2, 0>(a, stream);
+    case 7: return launch_dir<int, 2, 1>(a, stream);
+    case 8: return launch_dir<int, 2, 2>(a, stream);
+    case 9: return launch_dir<int, 3, 0>(a, stream);
+    case 10: return launch_dir<int, 3, 1>(a, stream);
+    default: return launch_dir<int, 3, 2>(a, stream);
+  }
 }
 
 }  // namespace tcb

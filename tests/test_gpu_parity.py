@@ -435,6 +435,21 @@ def test_random_small_f32(seed):
 
 
 @pytest.mark.usefixtures("both_f32_paths")
+@pytest.mark.parametrize("spec", ["mn-mk-kn", "mn-km-nk", "mn-mk-nk", "mn-km-kn"])
+@pytest.mark.parametrize("mnk", [(260, 196, 100), (132, 388, 36), (516, 132, 260)])
+def test_f32_vector_gathers(spec, mnk):
+    """Lengths that are multiples of 4 with aligned bases: the plan proves every 16-byte vector
+    contiguous, so the tcgen05 kernel's vector gathers run (K vectors into the K-major layout,
+    M vectors into the [k][m] staging of A); ragged tiles in M, N and K."""
+    lc, la, lb = spec.split("-")
+    case = W.Case("f32vec_" + spec, lc, la, lb, dict(zip("mnk", mnk)), dtype=torch.float32,
+                  alpha=0.75, beta=-0.5, c_init="dist", seed=41)
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.usefixtures("both_small_paths")
 def test_f32_misaligned_views():
     g = torch.Generator().manual_seed(4)
