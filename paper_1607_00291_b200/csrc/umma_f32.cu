@@ -635,7 +635,8 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   // faster split; profiles/r01/ab_umma_sk.txt). TC_UMMA_SK=0 turns the tail off.
   const char* pe = getenv("TC_UMMA_SK");
   const bool sk = a.stream_k && !(pe && !strcmp(pe, "0"));
-  Sched sc = make_sched(T, KT, a.num_sms, sk, 70);
+  const char* pp = getenv("TC_UMMA_DPPCT");   // measurement override of the 70% threshold
+  Sched sc = make_sched(T, KT, a.num_sms, sk, pp ? atoi(pp) : 70);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, a.num_sms, false);
   sc.wave_sync = 0;
   const int grid = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
