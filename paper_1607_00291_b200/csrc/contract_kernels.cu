@@ -408,7 +408,11 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (choice == 1 && !args.f32)
     return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
   if (choice == 0 && args.f32 && umma_f32_enabled()) {
-    const int r = launch_umma_f32(args, stream);
+    // N = 256 form when neither operand has 16-byte vector gathers (TC_UMMA_FORM=128|256 forces)
+    const char* fe = getenv("TC_UMMA_FORM");
+    const bool vec = args.a_vec_all || (args.b_vec_k && args.b_vec_all);
+    const bool n256 = fe ? !strcmp(fe, "256") : !vec;
+    const int r = n256 ? launch_umma_f32_n256(args, stream) : launch_umma_f32(args, stream);
     if (r != 0) return r;
   }
   LaunchArgs a = args;

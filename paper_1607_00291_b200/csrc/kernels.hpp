@@ -58,6 +58,7 @@ int launch_tiny(const LaunchArgs& a, cudaStream_t stream);
 // fp32 on the tcgen05 tensor cores with the 3xTF32 split: umma_f32.cu (int32 offsets, K >= 1).
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_umma_f32(const LaunchArgs& a, cudaStream_t stream);
+int launch_umma_f32_n256(const LaunchArgs& a, cudaStream_t stream);   // element gathers only
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
 int launch_contract(const LaunchArgs& a, cudaStream_t stream);

@@ -33,8 +33,16 @@
 #include "kernels.hpp"
 #include "sched.cuh"
 
+// This file is compiled twice: as itself (N = 128 MMAs, one K step per chunk) and through
+// umma_f32_n256.cu (N = 256 form, four K steps per chunk, element gathers only), each in its own
+// namespace with its own launch entry.
+#ifndef TC_UMMA_NS
+#define TC_UMMA_NS umma
+#define TC_UMMA_LAUNCH launch_umma_f32
+#endif
+
 namespace tcb {
-namespace umma {
+namespace TC_UMMA_NS {
 
 using namespace dev;
 using namespace sched;
@@ -52,11 +60,27 @@ constexpr int BM = 128, BN = 128, BK = 32, STAGES = kTmemA ? 4 : 3;
 #define TC_UMMA_PW 4
 #endif
 constexpr int kPW = TC_UMMA_PW;            // producer warps (4 or 8)
-constexpr int kConv0 = kPW, kEpi0 = kPW + 4, kMmaW = kPW + 8;   // first warp of each role
-constexpr int kThreads = (kPW + 9) * 32;
+#ifndef TC_UMMA_CW
+#define TC_UMMA_CW 4
+#endif
+constexpr int kCW = TC_UMMA_CW;            // converter warps (4 or 8; 8: two per TMEM lane quarter)
+constexpr int kConv0 = kPW, kEpi0 = kPW + kCW, kMmaW = kEpi0 + 4;   // first warp of each role
+constexpr int kThreads = (kMmaW + 1) * 32;
 constexpr int kTile = (BK / 4) * (128 * 4 + 16);   // floats per operand tile (padded K chunks)
-// stage layout: [A hi (raw), A lo, B hi (raw), B lo], or [A raw, B hi (raw), B lo] with A in TMEM
-constexpr int kStage = (kTmemA ? 3 : 4) * kTile;
+// N = 256 form (TC_UMMA_N256=1, needs A in TMEM): per K = 8 one 128x256 MMA of A hi against
+// [B hi; B lo] (256 rows: hi rows, then lo rows, in every K chunk) gives Ahi.Bhi in accumulator
+// columns 0-127 and Ahi.Blo in 128-255, and one 128x128 MMA adds Alo.Bhi to columns 128-255:
+// two MMAs instead of three, and a 128x256 MMA costs about what a 128x128 one does
+// (tools/calib/umma_rate_test.cu: ~145 cycles each).
+#ifndef TC_UMMA_N256
+#define TC_UMMA_N256 0
+#endif
+constexpr bool kN256 = TC_UMMA_N256 && kTmemA;
+constexpr int kChunkB = kN256 ? 2 * 128 * 4 + 16 : 128 * 4 + 16;   // B's K-chunk stride (floats)
+constexpr int kTileB = (BK / 4) * kChunkB;
+// stage layout: [A hi (raw), A lo, B hi (raw), B lo], or [A raw, B hi (raw), B lo] with A in TMEM,
+// or [A raw, B (hi and lo rows interleaved per K chunk)] in the N = 256 form
+constexpr int kStage = kTmemA ? kTile + (kN256 ? kTileB : 2 * kTile) : 4 * kTile;
 constexpr int kOffAl = kTile, kOffBh = kTmemA ? kTile : 2 * kTile, kOffBl = kOffBh + kTile;
 constexpr int GROUP_M = 2;
 // The tensor core's fp32 accumulation is biased (it truncates): on one-signed data the relative
@@ -72,8 +96,10 @@ constexpr int kChunkSteps = TC_UMMA_CHUNK;   // K steps of BK per chunk
 // TMEM (512 columns): kChunkBufs chunk accumulators of BN columns, then the running sum; three
 // buffers give the epilogue two chunks of slack while it stores a finished tile
 // (two with A in TMEM, whose two 64-column slots -- hi, lo -- take the last 128 columns)
-constexpr int kChunkBufs = kTmemA ? 2 : 3;
-constexpr int kSumCol = kChunkBufs * BN;
+// (N = 256 form: one 256-column chunk accumulator, released as soon as the epilogue has read it)
+constexpr int kChunkBufs = kN256 ? 1 : (kTmemA ? 2 : 3);
+constexpr int kChunkCols = kN256 ? 2 * BN : BN;
+constexpr int kSumCol = kChunkBufs * kChunkCols;
 constexpr int kACol = kSumCol + BN, kASlots = 2;
 static_assert(kSumCol + BN + (kTmemA ? kASlots * 2 * BK : 0) <= 512, "TMEM columns");
 
@@ -85,13 +111,15 @@ __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u
 // gather writes in one instruction on different banks. (The MN-major tf32 operand mode left the
 // accumulator at zero on this part, tools/calib/umma_tf32_test.cu, so both operands are K-major.)
 constexpr int kChunk = 128 * 4 + 16;
+template <int CH = kChunk>
 __device__ __forceinline__ int tile_off(int r, int k) {
-  return (k >> 2) * kChunk + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
+  return (k >> 2) * CH + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
 }
 
+template <int CH = kChunk>
 __device__ __forceinline__ uint64_t make_desc(const float* base, int j) {   // MMA step j (K 8j..)
-  const uint32_t addr = smem_u32(base + j * 2 * kChunk);
-  const uint32_t lbo = kChunk * 4, sbo = 128;
+  const uint32_t addr = smem_u32(base + j * 2 * CH);
+  const uint32_t lbo = CH * 4, sbo = 128;
   uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
@@ -140,6 +168,22 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&u)[32
 #ifndef TC_UMMA_HI_TRUNC
 #define TC_UMMA_HI_TRUNC 1
 #endif
+template <int N>
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&u)[N]) {
+  static_assert(N == 16, "x16");
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};\n"
+      :: "r"(taddr), "r"(u[0]), "r"(u[1]), "r"(u[2]), "r"(u[3]), "r"(u[4]), "r"(u[5]),
+         "r"(u[6]), "r"(u[7]), "r"(u[8]), "r"(u[9]), "r"(u[10]), "r"(u[11]), "r"(u[12]),
+         "r"(u[13]), "r"(u[14]), "r"(u[15])
+      : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const uint32_t (&u)[N]) {
+  if constexpr (N == 32) tmem_st32(taddr, u);
+  else tmem_st16(taddr, u);
+}
 __device__ __forceinline__ float tf32_trunc(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
@@ -157,7 +201,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 //             matrices half-filled, on disjoint banks thanks to the K-chunk pad)
 // Either way 4 sectors per 128 bytes when the operand is contiguous (a K-run operand read with
 // the row mapping would touch 8).
-template <typename IDX, bool KR>
+template <typename IDX, bool KR, int CH = kChunk>
 struct Gather {
   static constexpr int RG = KR ? 4 : 8;               // rows per instruction
   static constexpr int KG = KR ? 8 : 4;               // K per instruction
@@ -194,7 +238,7 @@ struct Gather {
       const bool kin = k0 + kk < K;
 #pragma unroll
       for (int i = 0; i < NR; ++i)
-        cp_async4(sm + tile_off(row(w, i, l), kk), g + (ro[i] + ko[j]), kin && ((rv >> i) & 1u));
+        cp_async4(sm + tile_off<CH>(row(w, i, l), kk), g + (ro[i] + ko[j]), kin && ((rv >> i) & 1u));
     }
   }
 };
@@ -207,7 +251,7 @@ struct Gather {
 //  GatherVM: vectors along the rows (A only: 4 consecutive m at one k) into a [k][m] staging
 //            layout (row k = 128 floats) that the converter warps read column-wise into TMEM;
 //            one instruction = one k, 128 consecutive m
-template <typename IDX>
+template <typename IDX, int CH = kChunk>
 struct GatherVK {
   static constexpr int NR = 128 / 4 / kPW;           // row groups of 4 per warp
   IDX ro[NR];
@@ -233,7 +277,7 @@ struct GatherVK {
     const bool kin = k0 + kk < K;                    // K is a multiple of 4 here
 #pragma unroll
     for (int i = 0; i < NR; ++i)
-      cp_async16(sm + tile_off(row(w, i, l), kk), g + (ro[i] + ko), kin && ((rv >> i) & 1u));
+      cp_async16(sm + tile_off<CH>(row(w, i, l), kk), g + (ro[i] + ko), kin && ((rv >> i) & 1u));
   }
 };
 
@@ -265,11 +309,18 @@ struct GatherVM {
 };
 
 // operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors
-template <typename IDX, int MODE> struct GatherSel;
-template <typename IDX> struct GatherSel<IDX, 0> { using type = Gather<IDX, false>; };
-template <typename IDX> struct GatherSel<IDX, 1> { using type = Gather<IDX, true>; };
-template <typename IDX> struct GatherSel<IDX, 2> { using type = GatherVK<IDX>; };
-template <typename IDX> struct GatherSel<IDX, 3> { using type = GatherVM<IDX>; };
+template <typename IDX, int MODE, int CH = kChunk> struct GatherSel;
+template <typename IDX, int CH> struct GatherSel<IDX, 0, CH> { using type = Gather<IDX, false, CH>; };
+template <typename IDX, int CH> struct GatherSel<IDX, 1, CH> { using type = Gather<IDX, true, CH>; };
+template <typename IDX, int CH> struct GatherSel<IDX, 2, CH> { using type = GatherVK<IDX, CH>; };
+template <typename IDX, int CH> struct GatherSel<IDX, 3, CH> { using type = GatherVM<IDX>; };
+
+#ifdef TC_UMMA_PROF
+// measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
+#define PWAIT(slot, stmt) { const long long t0_ = clock64(); stmt; prof[slot] += clock64() - t0_; }
+#else
+#define PWAIT(slot, stmt) stmt
+#endif
 
 __device__ __forceinline__ void epi_sync() {   // the four epilogue warps only
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
@@ -294,10 +345,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kASlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef TC_UMMA_PROF
+  long long prof[6] = {0, 0, 0, 0, 0, 0};
+  const long long tstart = clock64();
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kPW * 32);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], kCW * 32);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < kChunkBufs; ++a) {
@@ -327,7 +382,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   if (warp < kPW) {
     // ---------------------------------- producers ----------------------------------
     typename GatherSel<IDX, A_MODE>::type ga;
-    typename GatherSel<IDX, B_MODE>::type gb;
+    typename GatherSel<IDX, B_MODE, kChunkB>::type gb;
     uint32_t it = 0;
     // K offsets depend on the K step only: those of the next step are fetched while this one's
     // copies are in flight, so the table reads stay off the producer's critical path
@@ -345,7 +400,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
       }
       for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
-        if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+        if (it >= STAGES) PWAIT(0, mbar_wait(&empty[s], ((it / STAGES) - 1) & 1));
         float* st = stage0 + s * kStage;
         ga.issue(st, A, kt * BK, K, warp, lane);
         gb.issue(st + kOffBh, B, kt * BK, K, warp, lane);
@@ -363,14 +418,26 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     while (wi.next(tile, kb, ke, sk)) {
       for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
-        mbar_wait(&full[s], (it / STAGES) & 1);
+        PWAIT(1, mbar_wait(&full[s], (it / STAGES) & 1));
         float* st = stage0 + s * kStage;
+        if constexpr (kN256) {
+          // B: lo rows next to the hi rows of every K chunk
+#pragma unroll
+          for (int i = t; i < (BK / 4) * 128; i += kCW * 32) {
+            float4* hi = reinterpret_cast<float4*>(st + kOffBh + (i >> 7) * kChunkB) + (i & 127);
+            const float4 x = *hi;
+            float4 h;
+            h.x = tf32_trunc(x.x); h.y = tf32_trunc(x.y); h.z = tf32_trunc(x.z); h.w = tf32_trunc(x.w);
+            hi[128] = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z),
+                                  tf32_rna(x.w - h.w));
+          }
+        } else {
 #pragma unroll
         for (int op = kTmemA ? 1 : 0; op < 2; ++op) {   // A (in smem), then B: hi, lo buffers
           float4* hi = reinterpret_cast<float4*>(st + (op ? kOffBh : 0));
           float4* lo = reinterpret_cast<float4*>(st + (op ? kOffBl : kOffAl));
 #pragma unroll
-          for (int i = t; i < kTile / 4; i += 128) {
+          for (int i = t; i < kTile / 4; i += kCW * 32) {
             const float4 x = hi[i];
             float4 h;
 #if TC_UMMA_HI_TRUNC
@@ -387,22 +454,26 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
                                 tf32_rna(x.w - h.w));
           }
         }
+        }
         if constexpr (kTmemA) {
           // A to tensor memory: this thread's row (TMEM lane 32 q + lane), 32 K values
-          const int q = warp - kConv0;
+          const int q = (warp - kConv0) & 3;
+          constexpr int KC = BK * 4 / kCW;           // K columns per converter warp (32 or 16)
+          const int kc0 = ((warp - kConv0) >> 2) * KC;
           const int row = 32 * q + lane;
           const uint32_t slot = it % kASlots;
-          if (it >= kASlots) mbar_wait(&aempty[slot], ((it / kASlots) - 1) & 1);
+          if (it >= kASlots) PWAIT(2, mbar_wait(&aempty[slot], ((it / kASlots) - 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          uint32_t h[32], lo[32];
+          uint32_t h[KC], lo[KC];
 #pragma unroll
-          for (int c = 0; c < BK / 4; ++c) {
+          for (int c = 0; c < KC / 4; ++c) {
+            const int k = kc0 + 4 * c;
             float4 x;
             if constexpr (A_MODE == 3) {   // [k][m] staging
-              x = make_float4(st[(4 * c) * BM + row], st[(4 * c + 1) * BM + row],
-                              st[(4 * c + 2) * BM + row], st[(4 * c + 3) * BM + row]);
+              x = make_float4(st[k * BM + row], st[(k + 1) * BM + row], st[(k + 2) * BM + row],
+                              st[(k + 3) * BM + row]);
             } else {
-              x = *reinterpret_cast<const float4*>(st + tile_off(row, 4 * c));
+              x = *reinterpret_cast<const float4*>(st + tile_off(row, k));
             }
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -412,9 +483,10 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               lo[4 * c + e] = __float_as_uint(tf32_rna(xs[e] - hv));
             }
           }
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + slot * 2 * BK);
-          tmem_st32(ta, h);
-          tmem_st32(ta + BK, lo);
+          const uint32_t ta =
+              tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kACol + slot * 2 * BK + kc0);
+          tmem_st_n(ta, h);
+          tmem_st_n(ta + BK, lo);
           asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         }
@@ -472,11 +544,36 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
 #endif
         }
-        mbar_wait(&tfull[cb], (ch / kChunkBufs) & 1);
+        PWAIT(3, mbar_wait(&tfull[cb], (ch / kChunkBufs) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
         for (int c0 = 0; c0 < 4; ++c0) {
           uint32_t u[32];
+          if constexpr (kN256) {
+            // chunk = main (columns 0-127) + correction (128-255); the chunk accumulator is free
+            // for the next chunk's MMAs as soon as its last columns are in registers
+            {
+              uint32_t v[32];
+              tmem_ld32(tmem + lanes + (uint32_t)(32 * c0), u);
+              tmem_ld32(tmem + lanes + (uint32_t)(BN + 32 * c0), v);
+              asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                u[i] = __float_as_uint(__uint_as_float(u[i]) + __uint_as_float(v[i]));
+            }
+            if (c0 == 3) {
+              asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+              mbar_arrive(&tempty[cb]);
+            }
+            if (c > 0) {
+              uint32_t t2[32];
+              tmem_ld32(tmem + lanes + (uint32_t)(kSumCol + 32 * c0), t2);
+              asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                u[i] = __float_as_uint(__uint_as_float(u[i]) + __uint_as_float(t2[i]));
+            }
+          } else {
           tmem_ld32(tmem + lanes + (uint32_t)(cb * BN + 32 * c0), u);
           if (c > 0) {
             uint32_t t2[32];
@@ -487,6 +584,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               u[i] = __float_as_uint(__uint_as_float(u[i]) + __uint_as_float(t2[i]));
           } else {
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          }
           }
           if (!last) {
             tmem_st32(tmem + lanes + (uint32_t)(kSumCol + 32 * c0), u);
@@ -525,7 +623,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        mbar_arrive(&tempty[cb]);           // chunk accumulator cb may be overwritten now
+        if constexpr (!kN256) mbar_arrive(&tempty[cb]);   // chunk accumulator cb is free now
       }
       if (split) {
         // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
@@ -555,6 +653,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #endif
   } else {
     // ---------------------------------- MMA issuer ---------------------------------
+    const uint32_t idesc256 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(2 * BN >> 3) << 17) |
+                              ((uint32_t)(BM >> 4) << 24);
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
     uint32_t it = 0, ch = 0;
@@ -566,18 +666,29 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         const bool chunk_end = j0 == kChunkSteps - 1 || kt == ke - 1;
         if (chunk_start) {
           const int cb = ch % kChunkBufs;
-          if (ch >= kChunkBufs) mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1);
+          if (ch >= kChunkBufs) PWAIT(4, mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          d = tmem + (uint32_t)(cb * BN);
+          d = tmem + (uint32_t)(cb * kChunkCols);
         }
         const int s = it % STAGES;
-        mbar_wait(&conv[s], (it / STAGES) & 1);
+        PWAIT(5, mbar_wait(&conv[s], (it / STAGES) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
           const float* st = stage0 + s * kStage;
           const float* bh = st + kOffBh;
           const float* bl = st + kOffBl;
-          if constexpr (kTmemA) {
+          if constexpr (kN256) {
+            const uint32_t slot = it % kASlots;
+            const uint32_t ah = tmem + (uint32_t)(kACol + slot * 2 * BK), al = ah + BK;
+#pragma unroll
+            for (int j = 0; j < BK / 8; ++j) {
+              const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
+              const uint64_t db = make_desc<kChunkB>(bh, j);
+              mma_tf32_ta(d, ah + 8 * j, db, idesc256, acc0);      // [Ahi.Bhi | Ahi.Blo]
+              mma_tf32_ta(d + BN, al + 8 * j, db, idesc, 1u);      // + Alo.Bhi
+            }
+            mma_commit(&aempty[slot]);                 // A slot free once these complete
+          } else if constexpr (kTmemA) {
             const uint32_t slot = it % kASlots;
             const uint32_t ah = tmem + (uint32_t)(kACol + slot * 2 * BK), al = ah + BK;
 #pragma unroll
@@ -608,6 +719,11 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     }
   }
 
+#ifdef TC_UMMA_PROF
+  if (blockIdx.x == 0 && lane == 0)
+    printf("PROF warp %d total %lld empty %lld full %lld aempty %lld tfull %lld tempty %lld conv %lld\n",
+           warp, clock64() - tstart, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   if (warp == kMmaW) {
@@ -649,7 +765,7 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-}  // namespace umma
+}  // namespace TC_UMMA_NS
 
 // fp32 through the tensor cores (3xTF32). Applies to int32-offset fp32 contractions with
 // K >= 1. The gather of each operand follows its leading direction (plan.cpp: A is read along M
@@ -657,11 +773,24 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
 // contiguous and aligned (a_vec_all / b_vec_all); an N-contiguous B is always element-gathered
 // (its vectors would not be contiguous in the K-major MMA layout).
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
-int launch_umma_f32(const LaunchArgs& a, cudaStream_t stream) {
+int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   if (!a.f32 || a.idx64 || a.K < 1) return 0;
+#ifdef TC_UMMA_ELEM_ONLY
+  const int am = a.a_vec_m ? 0 : 1;
+  const int bm = a.b_vec_k ? 1 : 0;
+#else
   const int am = a.a_vec_m ? (a.a_vec_all ? 3 : 0) : (a.a_vec_all ? 2 : 1);
   const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : 1) : 0;
-  using namespace umma;
+#endif
+  using namespace TC_UMMA_NS;
+#ifdef TC_UMMA_ELEM_ONLY
+  switch (am * 3 + bm) {
+    case 0: return launch_dir<int, 0, 0>(a, stream);
+    case 1: return launch_dir<int, 0, 1>(a, stream);
+    case 3: return launch_dir<int, 1, 0>(a, stream);
+    default: return launch_dir<int, 1, 1>(a, stream);
+  }
+#endif
   switch (am * 3 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
     case 1: return launch_dir<int, 0, 1>(a, stream);

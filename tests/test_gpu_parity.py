@@ -31,11 +31,17 @@ def tc():
     return m
 
 
-@pytest.fixture(params=["0", "1"], ids=["ffma", "umma"])
+@pytest.fixture(params=["0", "1", "128", "256"], ids=["ffma", "umma", "umma128", "umma256"])
 def both_f32_paths(request, monkeypatch):
-    """fp32 cases through the FFMA2 kernel and, with TC_F32_UMMA=1, the tcgen05 3xTF32 kernel
-    (umma_f32.cu); the library reads TC_F32_UMMA on every call."""
-    monkeypatch.setenv("TC_F32_UMMA", request.param)
+    """fp32 cases through the FFMA2 kernel (TC_F32_UMMA=0) and the tcgen05 3xTF32 kernel in the
+    form the library picks (N = 256 unless an operand has vector gathers) and in each form
+    forced (TC_UMMA_FORM); the library reads both variables on every call."""
+    if request.param == "0":
+        monkeypatch.setenv("TC_F32_UMMA", "0")
+    else:
+        monkeypatch.setenv("TC_F32_UMMA", "1")
+        if request.param != "1":
+            monkeypatch.setenv("TC_UMMA_FORM", request.param)
     return request.param
 
 
