@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-gemm", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--distribute", default="slabs", choices=["slabs", "broadcast"],
+                    help="N>1 operand distribution: per-rank slabs (send/recv) or full broadcast")
     return ap.parse_args()
 
 
@@ -261,33 +263,45 @@ def run_native(args):
     spec, lens = case.spec, case.lens
     stream = torch.cuda.current_stream()
 
-    # -- inputs: seeded on rank 0's GPU, broadcast once over NCCL (the one exchange step)
+    # -- inputs: seeded on rank 0's GPU and distributed once over NCCL (the one exchange step):
+    # by default each rank receives only the A and B slabs its block of C reads (point-to-point,
+    # dist.distribute_slabs); --distribute broadcast sends everyone the full operands instead
     t_b0 = time.perf_counter()
+    slabs = world > 1 and args.distribute == "slabs"
+    A = B = None
     if rank == 0:
         A, B, _ = W.make_tensors(case, "cuda")
-    else:
+    elif not slabs:
         A = W.colmajor_view(torch.empty(math.prod(case.shape(case.lab_a)), dtype=torch.float64,
                                         device="cuda"), case.shape(case.lab_a))
         B = W.colmajor_view(torch.empty(math.prod(case.shape(case.lab_b)), dtype=torch.float64,
                                         device="cuda"), case.shape(case.lab_b))
     bcast_ms = None
+    recv_elems = None
+    ranges = tdist.shard_ranges(world, rank, lens, SHARD_LABELS) if world > 1 else {}
     if world > 1:
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        flatA = torch.as_strided(A, (A.numel(),), (1,))
-        flatB = torch.as_strided(B, (B.numel(),), (1,))
-        tdist.broadcast_operands([flatA, flatB], 0)
+        if slabs:
+            As, Bs, recv_elems = tdist.distribute_slabs(spec, A, B, lens, SHARD_LABELS, world,
+                                                        rank, dtype=torch.float64, device="cuda")
+            A = B = None   # rank 0 keeps dense copies of its own slabs, like every other rank
+        else:
+            flatA = torch.as_strided(A, (A.numel(),), (1,))
+            flatB = torch.as_strided(B, (B.numel(),), (1,))
+            tdist.broadcast_operands([flatA, flatB], 0)
         e1.record()
         torch.cuda.synchronize()
         bcast_ms = e0.elapsed_time(e1)
-    ranges = tdist.shard_ranges(world, rank, lens, SHARD_LABELS) if world > 1 else {}
+        torch.cuda.empty_cache()
     cshape = tdist.shard_shape(case.lab_c, lens, ranges)
     C = W.colmajor_view(torch.full((math.prod(cshape),), float("nan"), dtype=torch.float64,
                                    device="cuda"), cshape)
-    As = tdist.narrow(A, case.lab_a, ranges)
-    Bs = tdist.narrow(B, case.lab_b, ranges)
+    if not slabs:
+        As = tdist.narrow(A, case.lab_a, ranges)
+        Bs = tdist.narrow(B, case.lab_b, ranges)
     flops_rank = tdist.shard_flops(spec, lens, ranges)
     flops_total = case.flops()
     plan = tc.Plan.for_tensors(spec, As, Bs, C)
@@ -393,9 +407,11 @@ def run_native(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": case.name, "spec": spec, "lens": lens,
                    "mnk": [info["m"], info["n"], info["k"]], "flops_per_step": flops_total,
-                   "parallelism": f"shard C over ({SHARD_LABELS}) x{world}, NCCL broadcast of A,B",
+                   "parallelism": f"shard C over ({SHARD_LABELS}) x{world}, " + (
+                       "NCCL send/recv of per-rank A,B slabs" if slabs else "NCCL broadcast of A,B"),
                    "shard_ranges_rank0": ranges, "l2": "inputs larger than L2 (30.6 GB >> 126 MB)",
-                   "broadcast_ms": bcast_ms, "plan": info},
+                   "distribute": args.distribute if world > 1 else None,
+                   "distribute_ms": bcast_ms, "received_elems_rank": recv_elems, "plan": info},
         "pct_fp64_peak": round(100 * value / 1e3 / (peak * world), 2),
         "same_size_gemm": None if gemm_tf is None else {
             "kind": "cuBLAS DGEMM (torch.mm float64) of the rank-0 shard's M x N x K",

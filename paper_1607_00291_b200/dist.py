@@ -2,9 +2,11 @@
 
 Free (I/J) blocks of C are independent: partitioning is a sub-range of the scatter vectors
  and the K loop is never split, so ranks never reduce. The only
-collective is the initial NCCL broadcast of A and B from rank 0 (torch.distributed, NVLink).
-Each rank then contracts its shard with zero-copy sub-views of A and B (base pointer + narrowed
-lengths) into its own C shard, through the same C ABI call as one GPU.
+exchange is the initial distribution of A and B from rank 0 (torch.distributed over NCCL/NVLink):
+either a broadcast of the full operands (each rank then contracts zero-copy sub-views, base
+pointer + narrowed lengths) or, with less volume, point-to-point slabs holding just what each
+rank's block of C reads (distribute_slabs). Either way each rank contracts into its own C shard
+through the same C ABI call as one GPU.
 """
 from __future__ import annotations
 
@@ -78,3 +80,61 @@ def contract_shard(spec: str, A, B, C_shard, ranges, alpha: float, beta: float,
         contract_fn = tc.contract
     lc, la, lb = spec.split("-")
     return contract_fn(spec, narrow(A, la, ranges), narrow(B, lb, ranges), C_shard, alpha, beta)
+
+
+def _order_slowest_first(t) -> List[int]:
+    """Dims of t ordered by decreasing stride (its memory order, outermost first)."""
+    return sorted(range(t.dim()), key=lambda d: -abs(t.stride(d)))
+
+
+def distribute_slabs(spec: str, A, B, lens: Dict[str, int], shard_labels: str, world: int,
+                     rank: int, dtype=None, device=None, order_a: Sequence[int] = None,
+                     order_b: Sequence[int] = None, src: int = 0):
+    """Lower-volume operand distribution: instead of broadcasting the full
+    A and B, rank `src` sends every rank only the slabs its block of C reads -- A and B narrowed
+    to that rank's ranges of the shard labels they carry -- each as one dense tensor
+    over point-to-point send/recv. The slabs keep the operands' memory order (`order_a/b`: dims
+    outermost first; default column-major, the workloads' layout). `src` keeps dense copies of
+    its own slabs too, so every rank contracts the same layout. Returns (A_slab, B_slab,
+    elements received by this rank). A and B are only read on `src` (None elsewhere)."""
+    import torch
+    import torch.distributed as dist
+    lc, la, lb = spec.split("-")
+
+    def order(T, given, labels):
+        if given is not None:
+            return list(given)
+        if T is not None:
+            return _order_slowest_first(T)
+        return list(reversed(range(len(labels))))
+
+    oa, ob = order(A, order_a, la), order(B, order_b, lb)
+
+    def dense(view, o):
+        inv = sorted(range(len(o)), key=lambda i: o[i])
+        base = view.permute(*o).contiguous()
+        return base, base.permute(*inv)
+
+    def empty(labels, rg, o):
+        shape = shard_shape(labels, lens, rg)
+        base = torch.empty([shape[d] for d in o], dtype=dtype, device=device)
+        inv = sorted(range(len(o)), key=lambda i: o[i])
+        return base, base.permute(*inv)
+
+    mine = shard_ranges(world, rank, lens, shard_labels)
+    if rank == src:
+        for r in range(world):
+            if r == src:
+                continue
+            rg = shard_ranges(world, r, lens, shard_labels)
+            for T, labels, o in ((A, la, oa), (B, lb, ob)):
+                base, _ = dense(narrow(T, labels, rg), o)
+                dist.send(base, r)
+        _, a_mine = dense(narrow(A, la, mine), oa)
+        _, b_mine = dense(narrow(B, lb, mine), ob)
+        return a_mine, b_mine, 0
+    abase, a_mine = empty(la, mine, oa)
+    bbase, b_mine = empty(lb, mine, ob)
+    dist.recv(abase, src)
+    dist.recv(bbase, src)
+    return a_mine, b_mine, abase.numel() + bbase.numel()

@@ -95,3 +95,55 @@ def test_gloo_world2_sharded_equals_single(world):
         p.join(timeout=300)
         assert p.exitcode == 0
     assert q.get(timeout=10) is True
+
+
+def _worker_slabs(rank, world, port, q):
+    """Same protocol with the lower-volume distribution: rank 0 sends each rank only its A and
+    B slabs (dist.distribute_slabs); the shards must still assemble to the single result, and
+    each rank must have received exactly its slab volume."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        case = W.cfg5(big=6, small=4)
+        A = B = None
+        if rank == 0:
+            A, B, _ = W.make_tensors(case, "cpu")
+        As, Bs, got = tdist.distribute_slabs(case.spec, A, B, case.lens, "abc", world, rank,
+                                             dtype=torch.float64, device="cpu")
+        rg = tdist.shard_ranges(world, rank, case.lens, "abc")
+        expect = (math.prod(tdist.shard_shape(case.lab_a, case.lens, rg)) +
+                  math.prod(tdist.shard_shape(case.lab_b, case.lens, rg)))
+        cshape = tdist.shard_shape(case.lab_c, case.lens, rg)
+        C = W.colmajor_view(torch.full((math.prod(cshape),), float("nan"), dtype=torch.float64),
+                            cshape)
+        _oracle_contract(case.spec, As, Bs, C, case.alpha, case.beta)
+        shards = [None] * world
+        dist.all_gather_object(shards, (rg, C.contiguous().numpy(), got, expect))
+        if rank == 0:
+            full = W.make_tensors(case, "cpu")
+            ref = full[2].clone()
+            _oracle_contract(case.spec, full[0], full[1], ref, case.alpha, case.beta)
+            out = np.full(ref.shape, np.nan)
+            ok = True
+            for r, (g, c, n_got, n_exp) in enumerate(shards):
+                out[g["a"][0]:g["a"][1], g["b"][0]:g["b"][1], g["c"][0]:g["c"][1]] = c
+                ok &= (n_got == (0 if r == 0 else n_exp))
+                # less than the full operands whenever the rank's block is a proper sub-block
+                ok &= n_exp < full[0].numel() + full[1].numel()
+            q.put(bool(ok and np.array_equal(out, ref.numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_slab_distribution_equals_single(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_slabs, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True

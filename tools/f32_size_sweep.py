@@ -1,5 +1,6 @@
-"""fp32 contraction time over square-ish sizes for the current fp32 path (TC_F32_UMMA=0/1), next
-to SGEMM of equal M, N, K; CUDA graphs of 20 calls, one JSON line per size.
+"""Contraction time over square-ish GEMM-layout sizes for the current fp32 path (TC_F32_UMMA=0/1)
+or fp64 (SWEEP_DTYPE=f64), next to cuBLAS of equal M, N, K; CUDA graphs of 20 calls, one JSON
+line per size.
 
     TC_F32_UMMA=0 python tools/f32_size_sweep.py
 """
@@ -41,16 +42,18 @@ def main():
              (4096, 4096, 64), (8192, 8192, 256), (256, 256, 65536)]
     if os.environ.get("SWEEP_SIZES"):   # e.g. "512x512x512,1024x1024x1024"
         sizes = [tuple(int(v) for v in t.split("x")) for t in os.environ["SWEEP_SIZES"].split(",")]
+    dt = torch.float64 if os.environ.get("SWEEP_DTYPE") == "f64" else torch.float32
     for m, n, k in sizes:
-        A = torch.randn(m, k, device="cuda")
-        B = torch.randn(k, n, device="cuda")
-        C = torch.empty(m, n, device="cuda")
+        A = torch.randn(m, k, device="cuda", dtype=dt)
+        B = torch.randn(k, n, device="cuda", dtype=dt)
+        C = torch.empty(m, n, device="cuda", dtype=dt)
         t = graph_ms(lambda: tc.contract("mn-mk-kn", A, B, C))
         tg = graph_ms(lambda: torch.mm(A, B, out=C))
         fl = 2.0 * m * n * k
-        print(json.dumps({"mnk": [m, n, k], "umma": os.environ.get("TC_F32_UMMA", "1"),
+        print(json.dumps({"mnk": [m, n, k], "dtype": str(dt).split(".")[-1],
+                          "umma": os.environ.get("TC_F32_UMMA", "1"),
                           "ms": round(t, 4), "tflops": round(fl / t / 1e9, 2),
-                          "sgemm_ms": round(tg, 4), "vs_sgemm": round(tg / t, 3)}), flush=True)
+                          "gemm_ms": round(tg, 4), "vs_gemm": round(tg / t, 3)}), flush=True)
 
 
 if __name__ == "__main__":
