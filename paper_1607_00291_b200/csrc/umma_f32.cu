@@ -526,6 +526,12 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         flag = flags + s_local;
       }
       const bool read_c = piece > 0 || beta != 0.0;
+      // C's column offsets for the tile, one per lane and 32-column group, fetched now so the
+      // final store does not start with a table round trip
+      IDX colv[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        colv[g] = n0 + 32 * g + lane < N ? __ldg(cC + n0 + 32 * g + lane) : 0;
 #ifdef TC_UMMA_TRACE
       unsigned long long tr0, tr1 = 0, tr2 = 0;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
@@ -594,7 +600,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             // instead of one dependent read per element
             const int nb = n0 + 32 * c0;
             const bool full = nb + 32 <= N;
-            const IDX col = (full || nb + lane < N) ? __ldg(cC + nb + lane) : 0;
+            const IDX col = c0 == 0 ? colv[0] : c0 == 1 ? colv[1] : c0 == 2 ? colv[2] : colv[3];
             // (no branch on the row: the shuffles need the whole warp)
             if (read_c) {
               float old[32];
