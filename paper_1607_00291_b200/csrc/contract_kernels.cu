@@ -296,13 +296,8 @@ int launch_f64(const LaunchArgs& a, cudaStream_t stream) {
   constexpr int smem =
       STAGES * (ALayout<A_VM>::STAGE + BLayout<B_VK>::STAGE) * (int)sizeof(double);
   auto kern = tc_dmma_f64_kernel<IDX, A_VM, B_VK>;
-  static bool attr_set = false;  // per-instantiation, per-process (same device family)
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return -1;
-    attr_set = true;
-  }
+  static std::atomic<int> attr[kMaxDevices];
+  if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   dim3 grid(tiles_m * tiles_n);
   kern<<<grid, NTHREADS, smem, stream>>>(

@@ -1006,13 +1006,8 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
   constexpr int smem = smem_bytes<T, A_VM, B_VK, IDX, FFMA>(STAGES);
   auto kern = tc_dmma_ws_kernel<T, IDX, A_VM, B_VK, A_MODE, B_MODE, FFMA>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return -1;
-    attr_set = true;
-  }
+  static std::atomic<int> attr[kMaxDevices];
+  if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int KT = (a.K + BK - 1) / BK;
   Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k);

@@ -1,6 +1,7 @@
 // Device-side interface between tc_api.cpp and contract_kernels.cu.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -62,5 +63,22 @@ int launch_umma_f32_n256(const LaunchArgs& a, cudaStream_t stream);   // element
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
 int launch_contract(const LaunchArgs& a, cudaStream_t stream);
+
+// The dynamic shared-memory opt-in (cudaFuncSetAttribute) applies to the kernel on the current
+// device, so it is tracked per device (the largest size set so far); one process may drive
+// several GPUs. Returns false on a CUDA error.
+constexpr int kMaxDevices = 64;
+template <typename K>
+inline bool ensure_dyn_smem(K kern, int smem, std::atomic<int> (&done)[kMaxDevices]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
+  if (done[dev].load(std::memory_order_acquire) >= smem) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return false;
+  int cur = done[dev].load(std::memory_order_relaxed);
+  while (cur < smem && !done[dev].compare_exchange_weak(cur, smem, std::memory_order_release)) {
+  }
+  return true;
+}
 
 }  // namespace tcb

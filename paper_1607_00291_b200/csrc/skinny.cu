@@ -229,13 +229,8 @@ static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
   const int smem = (a.KP * (a.NP + 4) + NBUF * a.KP * kXP) * (int)sizeof(double) +
                    (a.KP + a.NP) * (int)sizeof(IDX);
   auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW, NBUF>;
-  static int attr = 0;
-  if (attr < smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return -1;
-    attr = smem;
-  }
+  static std::atomic<int> attr[kMaxDevices];
+  if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int nblk = (a.R + kRows - 1) / kRows;
   const int grid = nblk < nsm ? nblk : nsm;
   kern<<<grid, kThreads, smem, s>>>(a);

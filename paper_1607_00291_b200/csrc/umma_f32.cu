@@ -743,12 +743,8 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   constexpr int smem =
       STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs + kASlots) * 8 + 16;
   auto kern = tc_umma_f32_kernel<IDX, A_MODE, B_MODE>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  static std::atomic<int> attr[kMaxDevices];
+  if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int KT = (a.K + BK - 1) / BK;
   const int T = tiles_m * tiles_n;
