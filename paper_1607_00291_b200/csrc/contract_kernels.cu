@@ -407,7 +407,10 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
     const char* fe = getenv("TC_UMMA_FORM");
     const bool vec = args.a_vec_all || (args.b_vec_k && args.b_vec_all);
     const bool n256 = fe ? !strcmp(fe, "256") : !vec;
-    const int r = n256 ? launch_umma_f32_n256(args, stream) : launch_umma_f32(args, stream);
+    const bool pair = fe && !strcmp(fe, "pair");
+    const int r = pair   ? launch_umma_f32_pair(args, stream)
+                  : n256 ? launch_umma_f32_n256(args, stream)
+                         : launch_umma_f32(args, stream);
     if (r != 0) return r;
   }
   LaunchArgs a = args;

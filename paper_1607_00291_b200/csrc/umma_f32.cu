@@ -76,12 +76,22 @@ constexpr int kTile = (BK / 4) * (128 * 4 + 16);   // floats per operand tile (p
 #define TC_UMMA_N256 0
 #endif
 constexpr bool kN256 = TC_UMMA_N256 && kTmemA;
-constexpr int kChunkB = kN256 ? 2 * 128 * 4 + 16 : 128 * 4 + 16;   // B's K-chunk stride (floats)
+// CTA-pair form (TC_UMMA_PAIR=1, N = 128 form with A in TMEM): two CTAs of a cluster run one
+// 256 x 128 tile with tcgen05.mma.cta_group::2 (M = 256) issued by the leader; each CTA stages its
+// 128 rows of A (in its own TMEM) and half of B (64 rows), so one MMA instruction does twice the
+// work and each SM gathers and converts a quarter less.
+#ifndef TC_UMMA_PAIR
+#define TC_UMMA_PAIR 0
+#endif
+constexpr bool kPair = TC_UMMA_PAIR && kTmemA && !kN256;
+constexpr int kRowsB = kPair ? 64 : 128;    // B rows (N) staged per CTA
+constexpr int kTM = kPair ? 256 : 128;      // rows of C per tile
+constexpr int kChunkB = kN256 ? 2 * 128 * 4 + 16 : kRowsB * 4 + 16;   // B's K-chunk stride (floats)
 constexpr int kTileB = (BK / 4) * kChunkB;
 // stage layout: [A hi (raw), A lo, B hi (raw), B lo], or [A raw, B hi (raw), B lo] with A in TMEM,
 // or [A raw, B (hi and lo rows interleaved per K chunk)] in the N = 256 form
-constexpr int kStage = kTmemA ? kTile + (kN256 ? kTileB : 2 * kTile) : 4 * kTile;
-constexpr int kOffAl = kTile, kOffBh = kTmemA ? kTile : 2 * kTile, kOffBl = kOffBh + kTile;
+constexpr int kStage = kTmemA ? kTile + (kN256 ? kTileB : 2 * kTileB) : 4 * kTile;
+constexpr int kOffAl = kTile, kOffBh = kTmemA ? kTile : 2 * kTile, kOffBl = kOffBh + kTileB;
 constexpr int GROUP_M = 2;
 // The tensor core's fp32 accumulation is biased (it truncates): on one-signed data the relative
 // error grows with the number of MMAs chained into one accumulator (3xTF32, K = 128 per
@@ -201,11 +211,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
 //             matrices half-filled, on disjoint banks thanks to the K-chunk pad)
 // Either way 4 sectors per 128 bytes when the operand is contiguous (a K-run operand read with
 // the row mapping would touch 8).
-template <typename IDX, bool KR, int CH = kChunk>
+template <typename IDX, bool KR, int CH = kChunk, int ROWS = 128>
 struct Gather {
   static constexpr int RG = KR ? 4 : 8;               // rows per instruction
   static constexpr int KG = KR ? 8 : 4;               // K per instruction
-  static constexpr int NR = 128 / RG / kPW;           // row groups per warp
+  static constexpr int NR = ROWS / RG / kPW;          // row groups per warp
   static constexpr int NK = BK / KG;                  // K groups per stage
   IDX ro[NR];
   uint32_t rv;
@@ -251,9 +261,9 @@ struct Gather {
 //  GatherVM: vectors along the rows (A only: 4 consecutive m at one k) into a [k][m] staging
 //            layout (row k = 128 floats) that the converter warps read column-wise into TMEM;
 //            one instruction = one k, 128 consecutive m
-template <typename IDX, int CH = kChunk>
+template <typename IDX, int CH = kChunk, int ROWS = 128>
 struct GatherVK {
-  static constexpr int NR = 128 / 4 / kPW;           // row groups of 4 per warp
+  static constexpr int NR = ROWS / 4 / kPW;          // row groups of 4 per warp
   IDX ro[NR];
   uint32_t rv;
   IDX ko;
@@ -309,11 +319,11 @@ struct GatherVM {
 };
 
 // operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors
-template <typename IDX, int MODE, int CH = kChunk> struct GatherSel;
-template <typename IDX, int CH> struct GatherSel<IDX, 0, CH> { using type = Gather<IDX, false, CH>; };
-template <typename IDX, int CH> struct GatherSel<IDX, 1, CH> { using type = Gather<IDX, true, CH>; };
-template <typename IDX, int CH> struct GatherSel<IDX, 2, CH> { using type = GatherVK<IDX, CH>; };
-template <typename IDX, int CH> struct GatherSel<IDX, 3, CH> { using type = GatherVM<IDX>; };
+template <typename IDX, int MODE, int CH = kChunk, int ROWS = 128> struct GatherSel;
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 0, CH, R> { using type = Gather<IDX, false, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 1, CH, R> { using type = Gather<IDX, true, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 2, CH, R> { using type = GatherVK<IDX, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 3, CH, R> { using type = GatherVM<IDX>; };
 
 #ifdef TC_UMMA_PROF
 // measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
@@ -324,6 +334,39 @@ template <typename IDX, int CH> struct GatherSel<IDX, 3, CH> { using type = Gath
 
 __device__ __forceinline__ void epi_sync() {   // the four epilogue warps only
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
+}
+
+// cluster (CTA pair) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n"
+               ::: "memory");
+}
+// arrive on the barrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" :: "r"(r) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\nWAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITC_%=;\n}\n" :: "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ta_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t db,
+                                                 uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+               " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n"
+               :: "r"(tmem_d), "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {   // to both CTAs' barrier
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster"
+               ".b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "h"((uint16_t)3) : "memory");
 }
 
 template <typename IDX, int A_MODE, int B_MODE>
@@ -349,40 +392,48 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   const long long tstart = clock64();
 #endif
+  const uint32_t crank = kPair ? cluster_rank() : 0;   // 0: the pair's leader (issues the MMAs)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kPW * 32);
-      mbar_init(&conv[s], kCW * 32);
+      mbar_init(&conv[s], (kPair ? 2 : 1) * kCW * 32);   // pair: both CTAs' converters
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < kChunkBufs; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], (kPair ? 2 : 1) * 128);
     }
     for (int a = 0; a < kASlots; ++a) mbar_init(&aempty[a], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == kMmaW) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
-                 :: "r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                   :: "r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n"
+                   :: "r"(smem_u32(tmem_slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();   // barriers of both CTAs initialised, TMEM allocated
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   // every role walks the same work items: whole tiles, then this CTA's stream-K pieces
   // (sched.cuh); a piece is the K-step range [kb, ke) of one tile
   WorkIter wi;
-  wi.init(sched, blockIdx.x);
+  wi.init(sched, kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x);   // pair: one unit per cluster
   int tile, kb, ke;
   bool sk;
 
   if (warp < kPW) {
     // ---------------------------------- producers ----------------------------------
     typename GatherSel<IDX, A_MODE>::type ga;
-    typename GatherSel<IDX, B_MODE, kChunkB>::type gb;
+    typename GatherSel<IDX, B_MODE, kChunkB, kRowsB>::type gb;
     uint32_t it = 0;
     // K offsets depend on the K step only: those of the next step are fetched while this one's
     // copies are in flight, so the table reads stay off the producer's critical path
@@ -392,8 +443,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
-      ga.init(rA, tm * BM, M, warp, lane);
-      gb.init(cB, tn * BN, N, warp, lane);
+      ga.init(rA, tm * kTM + BM * (int)crank, M, warp, lane);
+      gb.init(cB, tn * BN + kRowsB * (int)crank, N, warp, lane);
       if (kpre != kb) {
         ga.load_k(cA, kb * BK, lane);
         gb.load_k(rB, kb * BK, lane);
@@ -437,7 +488,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           float4* hi = reinterpret_cast<float4*>(st + (op ? kOffBh : 0));
           float4* lo = reinterpret_cast<float4*>(st + (op ? kOffBl : kOffAl));
 #pragma unroll
-          for (int i = t; i < kTile / 4; i += kCW * 32) {
+          for (int i = t; i < (op ? kTileB : kTile) / 4; i += kCW * 32) {
             const float4 x = hi[i];
             float4 h;
 #if TC_UMMA_HI_TRUNC
@@ -491,7 +542,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the MMA
-        mbar_arrive(&conv[s]);
+        if constexpr (kPair) mbar_arrive_remote(&conv[s], 0);   // the leader's barrier
+        else mbar_arrive(&conv[s]);
       }
     }
   } else if (warp < kMmaW) {
@@ -508,7 +560,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     while (wi.next(tile, kb, ke, sk)) {
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
-      const int m = tm * BM + row;
+      const int m = tm * kTM + BM * (int)crank + row;
       const bool min_ = m < M;
       const IDX rc = min_ ? rC[m] : 0;
       const int n0 = tn * BN;
@@ -522,7 +574,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         const int s_local = tile - sched.D;
         const long long g_first = (long long)s_local * sched.KT;
         const int owner = (int)(((g_first + 1) * sched.P_sk + sched.I - 1) / sched.I) - 1;
-        piece = blockIdx.x - owner;
+        piece = (kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x) - owner;
         flag = flags + s_local;
       }
       const bool read_c = piece > 0 || beta != 0.0;
@@ -543,8 +595,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #ifdef TC_UMMA_TRACE
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
 #endif
+          // pair: each piece is published by both CTAs (two counts per piece)
           if (threadIdx.x == kEpi0 * 32)
-            while (ld_acquire(flag) != piece) __nanosleep(64);
+            while (ld_acquire(flag) != (kPair ? 2 * piece : piece)) __nanosleep(64);
           epi_sync();
 #ifdef TC_UMMA_TRACE
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
@@ -569,7 +622,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             }
             if (c0 == 3) {
               asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-              mbar_arrive(&tempty[cb]);
+              if constexpr (kPair) mbar_arrive_remote(&tempty[cb], 0);
+              else mbar_arrive(&tempty[cb]);
             }
             if (c > 0) {
               uint32_t t2[32];
@@ -629,7 +683,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        if constexpr (!kN256) mbar_arrive(&tempty[cb]);   // chunk accumulator cb is free now
+        if constexpr (kPair) mbar_arrive_remote(&tempty[cb], 0);   // chunk cb is free now
+        else if constexpr (!kN256) mbar_arrive(&tempty[cb]);
       }
       if (split) {
         // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
@@ -637,7 +692,13 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         epi_sync();
         if (threadIdx.x == kEpi0 * 32) {
           __threadfence();
-          st_release(flag, ke < sched.KT ? piece + 1 : 0);
+          if constexpr (kPair) {
+            // count this half; the second half of the last piece resets the flag
+            const int old = atomicAdd(flag, 1);
+            if (ke == sched.KT && old == 2 * piece + 1) st_release(flag, 0);
+          } else {
+            st_release(flag, ke < sched.KT ? piece + 1 : 0);
+          }
         }
       }
 #ifdef TC_UMMA_TRACE
@@ -662,9 +723,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     const uint32_t idesc256 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(2 * BN >> 3) << 17) |
                               ((uint32_t)(BM >> 4) << 24);
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)(kTM >> 4) << 24);   // pair: M = 256 across the two CTAs
     uint32_t it = 0, ch = 0;
-    while (wi.next(tile, kb, ke, sk)) {
+    while ((!kPair || crank == 0) && wi.next(tile, kb, ke, sk)) {
       uint32_t d = 0;
       for (int kt = kb; kt < ke; ++kt, ++it) {
         const int j0 = (kt - kb) % kChunkSteps;
@@ -672,18 +733,34 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         const bool chunk_end = j0 == kChunkSteps - 1 || kt == ke - 1;
         if (chunk_start) {
           const int cb = ch % kChunkBufs;
-          if (ch >= kChunkBufs) PWAIT(4, mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
+          if (ch >= kChunkBufs) {
+            if constexpr (kPair) PWAIT(4, mbar_wait_cluster(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
+            else PWAIT(4, mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
+          }
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           d = tmem + (uint32_t)(cb * kChunkCols);
         }
         const int s = it % STAGES;
-        PWAIT(5, mbar_wait(&conv[s], (it / STAGES) & 1));
+        if constexpr (kPair) PWAIT(5, mbar_wait_cluster(&conv[s], (it / STAGES) & 1));
+        else PWAIT(5, mbar_wait(&conv[s], (it / STAGES) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
           const float* st = stage0 + s * kStage;
           const float* bh = st + kOffBh;
           const float* bl = st + kOffBl;
-          if constexpr (kN256) {
+          if constexpr (kPair) {
+            const uint32_t slot = it % kASlots;
+            const uint32_t ah = tmem + (uint32_t)(kACol + slot * 2 * BK), al = ah + BK;
+#pragma unroll
+            for (int j = 0; j < BK / 8; ++j) {
+              const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
+              const uint64_t dbh = make_desc<kChunkB>(bh, j), dbl = make_desc<kChunkB>(bl, j);
+              mma_tf32_ta_pair(d, ah + 8 * j, dbh, idesc, acc0);
+              mma_tf32_ta_pair(d, ah + 8 * j, dbl, idesc, 1u);
+              mma_tf32_ta_pair(d, al + 8 * j, dbh, idesc, 1u);
+            }
+            mma_commit_pair(&aempty[slot]);            // both CTAs' A slots are free
+          } else if constexpr (kN256) {
             const uint32_t slot = it % kASlots;
             const uint32_t ah = tmem + (uint32_t)(kACol + slot * 2 * BK), al = ah + BK;
 #pragma unroll
@@ -716,8 +793,13 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
             }
           }
-          mma_commit(&empty[s]);                       // stage s is free once these complete
-          if (chunk_end) mma_commit(&tfull[ch % kChunkBufs]);   // this chunk's accumulator is complete
+          if constexpr (kPair) {
+            mma_commit_pair(&empty[s]);
+            if (chunk_end) mma_commit_pair(&tfull[ch % kChunkBufs]);
+          } else {
+            mma_commit(&empty[s]);                     // stage s is free once these complete
+            if (chunk_end) mma_commit(&tfull[ch % kChunkBufs]);   // the chunk is complete
+          }
         }
         __syncwarp();
         if (chunk_end) ++ch;
@@ -731,10 +813,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
            warp, clock64() - tstart, prof[0], prof[1], prof[2], prof[3], prof[4], prof[5]);
 #endif
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();   // neither CTA frees TMEM the pair still uses
+  else __syncthreads();
   if (warp == kMmaW) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tmem));
+    if constexpr (kPair)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" :: "r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tmem));
   }
 }
 
@@ -745,25 +831,46 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   auto kern = tc_umma_f32_kernel<IDX, A_MODE, B_MODE>;
   static std::atomic<int> attr[kMaxDevices];
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
-  const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
+  const int tiles_m = (a.M + kTM - 1) / kTM, tiles_n = (a.N + BN - 1) / BN;
   const int KT = (a.K + BK - 1) / BK;
   const int T = tiles_m * tiles_n;
+  const int units = kPair ? a.num_sms / 2 : a.num_sms;   // schedule units: CTAs or CTA pairs
   // stream-K only when the partial wave is < 70% full: split pieces cost this kernel more than
   // the DMMA one (cfg4 fp32: a 74-86% partial wave ran 8-13% faster whole, a < 30% one 10-20%
   // faster split; profiles/r01/ab_umma_sk.txt). TC_UMMA_SK=0 turns the tail off.
   const char* pe = getenv("TC_UMMA_SK");
   const bool sk = a.stream_k && !(pe && !strcmp(pe, "0"));
   const char* pp = getenv("TC_UMMA_DPPCT");   // measurement override of the 70% threshold
-  Sched sc = make_sched(T, KT, a.num_sms, sk, pp ? atoi(pp) : 70);
-  if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, a.num_sms, false);
+  Sched sc = make_sched(T, KT, units, sk, pp ? atoi(pp) : 70);
+  if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, units, false);
   sc.wave_sync = 0;
-  const int grid = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
-  kern<<<grid, kThreads, smem, s>>>(
-      static_cast<const float*>(a.A), static_cast<const float*>(a.B), static_cast<float*>(a.C),
-      static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
-      static_cast<const IDX*>(a.rB), static_cast<const IDX*>(a.cB),
-      static_cast<const IDX*>(a.rC), static_cast<const IDX*>(a.cC), a.M, a.N, a.K, tiles_m,
-      tiles_n, a.alpha, a.beta, sc, a.flags);
+  const int nunits = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
+  const float* pA = static_cast<const float*>(a.A);
+  const float* pB = static_cast<const float*>(a.B);
+  float* pC = static_cast<float*>(a.C);
+  const IDX *trA = static_cast<const IDX*>(a.rA), *tcA = static_cast<const IDX*>(a.cA);
+  const IDX *trB = static_cast<const IDX*>(a.rB), *tcB = static_cast<const IDX*>(a.cB);
+  const IDX *trC = static_cast<const IDX*>(a.rC), *tcC = static_cast<const IDX*>(a.cC);
+  if constexpr (kPair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * nunits);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr1[1];
+    attr1[0].id = cudaLaunchAttributeClusterDimension;
+    attr1[0].val.clusterDim.x = 2;
+    attr1[0].val.clusterDim.y = 1;
+    attr1[0].val.clusterDim.z = 1;
+    cfg.attrs = attr1;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
+                           tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags) != cudaSuccess)
+      return -1;
+  } else {
+    kern<<<nunits, kThreads, smem, s>>>(pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
+                                        tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

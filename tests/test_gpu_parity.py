@@ -31,11 +31,12 @@ def tc():
     return m
 
 
-@pytest.fixture(params=["0", "1", "128", "256"], ids=["ffma", "umma", "umma128", "umma256"])
+@pytest.fixture(params=["0", "1", "128", "256", "pair"],
+                ids=["ffma", "umma", "umma128", "umma256", "ummapair"])
 def both_f32_paths(request, monkeypatch):
     """fp32 cases through the FFMA2 kernel (TC_F32_UMMA=0) and the tcgen05 3xTF32 kernel in the
     form the library picks (N = 256 unless an operand has vector gathers) and in each form
-    forced (TC_UMMA_FORM); the library reads both variables on every call."""
+    forced (TC_UMMA_FORM=128|256|pair); the library reads both variables on every call."""
     if request.param == "0":
         monkeypatch.setenv("TC_F32_UMMA", "0")
     else:
