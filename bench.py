@@ -407,8 +407,10 @@ def run_native(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": case.name, "spec": spec, "lens": lens,
                    "mnk": [info["m"], info["n"], info["k"]], "flops_per_step": flops_total,
-                   "parallelism": f"shard C over ({SHARD_LABELS}) x{world}, " + (
-                       "NCCL send/recv of per-rank A,B slabs" if slabs else "NCCL broadcast of A,B"),
+                   "parallelism": ("1 GPU, whole contraction" if world == 1 else
+                                   f"shard C over ({SHARD_LABELS}) x{world}, " + (
+                                       "NCCL send/recv of per-rank A,B slabs" if slabs
+                                       else "NCCL broadcast of A,B")),
                    "shard_ranges_rank0": ranges, "l2": "inputs larger than L2 (30.6 GB >> 126 MB)",
                    "distribute": args.distribute if world > 1 else None,
                    "distribute_ms": bcast_ms, "received_elems_rank": recv_elems, "plan": info},
