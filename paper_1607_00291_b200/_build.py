@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("TC_LIB_OUT") or os.path.join(HERE, "libtc_b200.so")
 OBJ = os.path.join(HERE, "build_obj") if not os.environ.get("TC_LIB_OUT") else LIB + ".obj"
 EXTRA = os.environ.get("TC_NVCC_EXTRA", "").split()
-SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "skinny.cu", "tiny.cu", "umma_f32.cu", "umma_f32_n256.cu", "umma_f32_pair.cu",
+SOURCES = ["plan.cpp", "tc_api.cpp", "contract_kernels.cu", "skinny.cu", "tiny.cu", "rankk.cu", "umma_f32.cu", "umma_f32_n256.cu", "umma_f32_pair.cu",
            "ws_f64_a0.cu", "ws_f64_a1.cu", "ws_f64_a2.cu",
            "ws_f32_ffma_a0.cu", "ws_f32_ffma_a1.cu", "ws_f32_ffma_a2.cu", "ws_f32_ffma_a3.cu",
            "ws_f32_dmma.cu"]

@@ -375,6 +375,13 @@ static int skinny_mode() {
   return 2;
 }
 
+// TC_RANKK=0 sends K <= 16 contractions with large free extents to the tile kernels instead
+// of the rank-k kernel (rankk.cu). Read on every call (tests cover both paths).
+static bool rankk_enabled() {
+  const char* e = getenv("TC_RANKK");
+  return !(e && !strcmp(e, "0"));
+}
+
 // TC_TINY=0 sends tiny contractions to the tensor-core kernel too (tests cover both paths).
 static bool tiny_enabled() {
   const char* e = getenv("TC_TINY");
@@ -394,6 +401,10 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   const int choice = kernel_choice();
   if (choice == 0 && tiny_enabled()) {
     const int r = launch_tiny(args, stream);
+    if (r != 0) return r;
+  }
+  if (choice == 0 && rankk_enabled()) {
+    const int r = launch_rankk(args, stream);
     if (r != 0) return r;
   }
   if (choice == 0 && skinny_mode() != 0) {

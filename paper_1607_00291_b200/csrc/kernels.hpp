@@ -61,6 +61,7 @@ int launch_tiny(const LaunchArgs& a, cudaStream_t stream);
 int launch_umma_f32(const LaunchArgs& a, cudaStream_t stream);
 int launch_umma_f32_n256(const LaunchArgs& a, cudaStream_t stream);   // element gathers only
 int launch_umma_f32_pair(const LaunchArgs& a, cudaStream_t stream);   // CTA pairs (cta_group::2)
+int launch_rankk(const LaunchArgs& a, cudaStream_t stream);   // K <= 16, large free extents
 
 // Number of kernel launches it made, or -1 on a CUDA error (cudaGetLastError holds it).
 int launch_contract(const LaunchArgs& a, cudaStream_t stream);

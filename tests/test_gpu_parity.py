@@ -575,6 +575,34 @@ def test_f2_fig_bench_full_sampled(idx):
     assert e < 1e-12
 
 
+@pytest.fixture(params=["1", "0"], ids=["rankk", "tile"])
+def both_rankk_paths(request, monkeypatch):
+    """K <= 16 contractions with large free extents through the rank-k kernel (rankk.cu) and,
+    with TC_RANKK=0, through the tile kernels; the library reads TC_RANKK on every call."""
+    monkeypatch.setenv("TC_RANKK", request.param)
+    return request.param
+
+
+@pytest.mark.usefixtures("both_rankk_paths")
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("mnk", [(2048, 2048, 5), (2100, 1037, 8), (4096, 1024, 1)])
+def test_rankk_kernel_shapes(mnk, dtype):
+    """Rank-k shapes (ragged column blocks, K = 1, 5, 8), beta != 0, both layouts, so that
+    C's unit stride sits in either free bundle (the kernel takes only C-rows-contiguous ones)."""
+    m, n, k = mnk
+    for spec in ("mn-mk-kn", "nm-km-nk"):
+        lc, la, lb = spec.split("-")
+        case = W.Case("rk_" + spec, lc, la, lb, {"m": m, "n": n, "k": k}, dtype=dtype,
+                      alpha=0.5, beta=-0.25, c_init="dist", seed=51)
+        Ad, Bd, Cd = W.make_tensors(case, "cuda")
+        C0 = Cd.clone()
+        tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+        e, c1, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=6, seed=k)
+        assert torch.isfinite(c1).all()
+        assert e < TOL[dtype]
+
+
+@pytest.mark.usefixtures("both_rankk_paths")
 @pytest.mark.parametrize("i", range(7))
 def test_f1_rankk_full_sampled(i):
     case = W.rankk(i)
