@@ -270,7 +270,9 @@ def run_native(args):
     slabs = world > 1 and args.distribute == "slabs"
     A = B = None
     if rank == 0:
-        A, B, _ = W.make_tensors(case, "cuda")
+        A, B, c_full = W.make_tensors(case, "cuda")
+        del c_full   # the timed C is this rank's shard, allocated below
+        torch.cuda.empty_cache()
     elif not slabs:
         A = W.colmajor_view(torch.empty(math.prod(case.shape(case.lab_a)), dtype=torch.float64,
                                         device="cuda"), case.shape(case.lab_a))
