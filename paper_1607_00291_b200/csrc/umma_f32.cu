@@ -1,27 +1,33 @@
 // fp32 contraction on the 5th-generation tensor cores (sm_100a tcgen05, kind::tf32) with the
 // 3xTF32 split: every fp32 operand x is split into hi = tf32(x) and lo = x - hi, and
 // A.B = Ahi.Bhi + Ahi.Blo + Alo.Bhi (the Alo.Blo term, ~2^-20 relative, is dropped), accumulated
-// in fp32 in tensor memory (reading R18 in DESIGN.md). Normwise error ~1e-6 on cfg4 (FFMA2
-// kernel: 0.7-1.1e-6), against the 1e-5 bound of BASELINE north_star checked by the parity tests.
+// in fp32 in tensor memory in chunks of K summed with rounded fp32 adds (reading R18 in
+// DESIGN.md). Normwise error <= 5e-7 on cfg4 at full size (FFMA2 kernel: <= 1.1e-6), against the
+// 1e-5 bound of BASELINE north_star checked by the parity tests.
 //
 // The paper's method is unchanged: the tiles are gathered from the tensors' strides through the
 // scatter vectors -- here straight into the tensor cores' canonical
-// shared-memory layout -- and C is written through its scatter vectors with alpha / beta
-// (P:605-616). One CTA per SM walks the persistent schedule of sched.cuh (whole 128 x 128 tiles
-// of C, then stream-K pieces fixed up in place):
-//   warps 0-3   producers: cp.async element gathers of A and B (128 x 32 each per K step) into
-//               the stage's hi buffers in the K-major canonical layout; each warp instruction
-//               fills one 128-byte core matrix (8 rows x 4 K), so shared-memory writes are
-//               conflict free and global reads come in 32-byte runs from an M/N-contiguous
-//               operand (8 rows) or 16-byte runs from a K-contiguous one (4 K)
-//   warps 4-7   converters: hi stays the raw fp32 value (the tensor core reads its tf32 bits,
-//               i.e. truncates); lo = rna(x - trunc(x)) goes to the stage's lo buffers
+// shared-memory layout, or for A on into tensor memory -- and C is written through its scatter
+// vectors with alpha / beta. One CTA per SM walks the persistent schedule of
+// sched.cuh (whole 128 x 128 tiles of C, then stream-K pieces fixed up in place). Default build
+// (A in TMEM, N = 128 MMAs, one K step per chunk):
+//   warps 0-3   producers: cp.async gathers of A and B (128 x 32 each per K step) into the stage:
+//               4-byte element copies laid out so a warp instruction reads whole 32-byte
+//               sectors of a contiguous operand (8 rows x 4 K or 4 rows x 8 K), or 16-byte
+//               vector copies where the plan proved the operand's vectors contiguous and aligned
+//   warps 4-7   converters: B's lo = rna(x - trunc(x)) next to B's raw value (the tensor core
+//               reads hi as the raw value's tf32 bits, i.e. truncated); A's hi and lo go to an
+//               A slot in tensor memory (one row per thread, tcgen05.st)
 //   warps 8-11  epilogue: tcgen05.ld of each chunk accumulator (warp w reads TMEM lanes
 //               32 (w - 8)..), added into the running sum in TMEM; at the end of a work item
 //               one row of C per thread, alpha * acc + beta * C through rscat_C / cscat_C
-//   warp 12     MMA issuer: one lane issues 3 x 4 tcgen05.mma (M = N = 128, K = 8) per K step and
-//               commits them to the stage's `empty` barrier; three TMEM chunk accumulators let
-//               the epilogue's adds overlap the next chunk's MMAs.
+//   warp 12     MMA issuer: one lane issues 3 x 4 tcgen05.mma (M = N = 128, K = 8, A from TMEM)
+//               per K step and commits them to the stage's, the A slot's and the chunk's
+//               barriers; two TMEM chunk accumulators let the epilogue's adds overlap the next
+//               chunk's MMAs.
+// Compile-time forms of the same source: TC_UMMA_N256 (umma_f32_n256.cu), TC_UMMA_PAIR
+// (umma_f32_pair.cu); measurement switches: TC_UMMA_TMEM_A, TC_UMMA_CHUNK, TC_UMMA_PW/CW,
+// TC_UMMA_HI_TRUNC, TC_UMMA_TRACE, TC_UMMA_PROF.
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -33,9 +39,9 @@
 #include "kernels.hpp"
 #include "sched.cuh"
 
-// This file is compiled twice: as itself (N = 128 MMAs, one K step per chunk) and through
-// umma_f32_n256.cu (N = 256 form, four K steps per chunk, element gathers only), each in its own
-// namespace with its own launch entry.
+// This file is compiled three times: as itself (N = 128 MMAs, one K step per chunk), through
+// umma_f32_n256.cu (N = 256 form, four K steps per chunk, element gathers only) and through
+// umma_f32_pair.cu (CTA pairs), each in its own namespace with its own launch entry.
 #ifndef TC_UMMA_NS
 #define TC_UMMA_NS umma
 #define TC_UMMA_LAUNCH launch_umma_f32
