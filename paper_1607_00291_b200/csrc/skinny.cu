@@ -232,7 +232,11 @@ static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
   static std::atomic<int> attr[kMaxDevices];
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int nblk = (a.R + kRows - 1) / kRows;
-  const int grid = nblk < nsm ? nblk : nsm;
+  // low arithmetic intensity (small resident operand, e.g. N = K = 32: HBM-bound) runs three
+  // CTAs per SM's worth of grid, more blocks in flight; larger ones one (f2 strings: N = K = 32
+  // 0.88 -> 0.98 of DGEMM, N = K = 76 -3..-5% with three; profiles/r01/ab_skinny_grid.txt)
+  const int cps = a.KP * a.NP <= 48 * 48 ? 3 : 1;
+  const int grid = nblk < cps * nsm ? nblk : cps * nsm;
   kern<<<grid, kThreads, smem, s>>>(a);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
