@@ -18,6 +18,7 @@
 // The operand layouts in shared memory follow the direction each operand is gathered along
 // (its unit-stride bundle), padded so that fragment loads are bank-conflict free.
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include <cuda_runtime.h>
@@ -1010,7 +1011,11 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int KT = (a.K + BK - 1) / BK;
-  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k);
+  static const int dp_pct = [] {   // measurement override of the 88% threshold (TC_WS_DPPCT)
+    const char* e = getenv("TC_WS_DPPCT");
+    return e ? atoi(e) : 88;
+  }();
+  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k, dp_pct);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) {   // cannot happen: S < 2 * num_sms
     Sched dp = make_sched(tiles_m * tiles_n, KT, a.num_sms, false);
     sc = dp;
