@@ -15,7 +15,10 @@ namespace tcb {
 namespace tiny {
 
 constexpr int kThreads = 128;   // consecutive m (C's unit-stride bundle)
-constexpr int kNB = 4;          // columns of C per thread (B values shared through smem)
+// columns of C per thread (B shared through smem): 2 while the grid stays within four CTAs per
+// SM, else 4 (cfg1 64^3: 5.3 -> 4.4 us; 512^2 x 64 prefers 4: 7.5 vs 10.9 us;
+// profiles/r01/tiny_sweep_nb.txt)
+constexpr int kNBMax = 4;
 constexpr int kMaxK = 256;
 
 // CTA = 128 consecutive rows x kNB columns of C. The CTA stages its kNB columns of B (K x kNB
@@ -25,7 +28,7 @@ constexpr int kMaxK = 256;
 // block of A is already in flight while B is being staged. Each A value feeds kNB
 // multiply-adds.
 constexpr int kKB = 32;
-template <typename T, typename IDX>
+template <typename T, typename IDX, int kNB>
 __global__ void __launch_bounds__(kThreads) tc_tiny_kernel(
     const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
     const IDX* __restrict__ rA, const IDX* __restrict__ cA, const IDX* __restrict__ rB,
@@ -74,16 +77,22 @@ __global__ void __launch_bounds__(kThreads) tc_tiny_kernel(
   }
 }
 
-template <typename T, typename IDX>
-static int launch_t(const LaunchArgs& a, cudaStream_t s) {
+template <typename T, typename IDX, int kNB>
+static int launch_nb(const LaunchArgs& a, cudaStream_t s) {
   const dim3 grid((a.M + kThreads - 1) / kThreads, (a.N + kNB - 1) / kNB);
-  tc_tiny_kernel<T, IDX><<<grid, kThreads, 0, s>>>(
+  tc_tiny_kernel<T, IDX, kNB><<<grid, kThreads, 0, s>>>(
       static_cast<const T*>(a.A), static_cast<const T*>(a.B), static_cast<T*>(a.C),
       static_cast<const IDX*>(a.rA), static_cast<const IDX*>(a.cA),
       static_cast<const IDX*>(a.rB), static_cast<const IDX*>(a.cB),
       static_cast<const IDX*>(a.rC), static_cast<const IDX*>(a.cC), a.M, a.N, a.K, a.alpha,
       a.beta);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+template <typename T, typename IDX>
+static int launch_t(const LaunchArgs& a, cudaStream_t s) {
+  const long long ctas2 = (long long)((a.M + kThreads - 1) / kThreads) * ((a.N + 1) / 2);
+  return ctas2 <= 4ll * a.num_sms ? launch_nb<T, IDX, 2>(a, s) : launch_nb<T, IDX, 4>(a, s);
 }
 
 }  // namespace tiny
@@ -94,9 +103,11 @@ static int launch_t(const LaunchArgs& a, cudaStream_t s) {
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int launch_tiny(const LaunchArgs& a, cudaStream_t stream) {
   const long long mn = (long long)a.M * a.N;
-  if (a.K > tiny::kMaxK || a.N > 65535 * tiny::kNB || mn > (1ll << a.tiny_mn_log2) ||
+  if (a.K > tiny::kMaxK || a.N > 65535 * tiny::kNBMax || mn > (1ll << a.tiny_mn_log2) ||
       mn * (a.K > 0 ? a.K : 1) > (1ll << a.tiny_mnk_log2))
     return 0;
+  // fp32 hands the top of the range to the tcgen05 kernel (256^3: 16 vs 22 us)
+  if (a.f32 && mn * (a.K > 0 ? a.K : 1) > (1ll << (a.tiny_mnk_log2 - 1))) return 0;
   if (a.f32)
     return a.idx64 ? tiny::launch_t<float, long long>(a, stream)
                    : tiny::launch_t<float, int>(a, stream);
