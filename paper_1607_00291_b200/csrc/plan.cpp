@@ -322,6 +322,17 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
           if ((int)i != u && (int)i != w) out.push_back(p->kb.P[i]);
         p->kb.P = out;
         p->k_blocked = true;
+      } else {
+        // A length with no divisor <= 4 (e.g. 323 = 17 * 19, fig:bench's ab-cad-dcb): if it is a
+        // single label and both dimensions are long, record a split of that label at the
+        // largest multiple of 4; the device entry point runs the divisible main part (which is
+        // then sub-divided) and the small remainder as separate contractions
+        const Dim& dx = bu == 1 ? du : dw;
+        const Dim& dy = bu == 1 ? dw : du;
+        if (dx.labels.size() == 1 && dx.len >= 64 && dy.len >= 64) {
+          p->split_label = dx.labels[0];
+          p->split_main = dx.len - dx.len % 4;
+        }
       }
     }
   }

@@ -81,6 +81,11 @@ struct Plan {
   // row blocking of the long free bundle for the skinny kernel (1, 1: none), see plan.cpp
   int skinny_bu = 1, skinny_bv = 1;
   bool k_blocked = false;   // P walked as [u_lo, w_lo, u_hi, w_hi, ...] (plan.cpp)
+  // sub-division blocked by a length without a small power-of-two divisor (plan.cpp): the
+  // contraction is run as a main part over split_label in [0, split_main), which can be
+  // sub-divided, plus the remainder (tc_api.cpp); 0 = no split
+  char split_label = 0;
+  int64_t split_main = 0;
   int variant = 0;
   // per-device uploaded tables
   mutable std::mutex mu;

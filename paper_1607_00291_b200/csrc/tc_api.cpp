@@ -567,6 +567,23 @@ using namespace tcb;
 
 extern "C" {
 
+// Restrict the bound label `lbl` of an operand to [lo, lo + len): same strides, shorter length,
+// data pointer moved to element lo along it (a zero-copy sub-view).
+static tc_tensor restrict_label(const tc_tensor* T, char lbl, int64_t lo, int64_t len, size_t esz,
+                                std::vector<int64_t>& lens) {
+  tc_tensor out = *T;
+  lens.assign(T->lens, T->lens + T->rank);
+  char* base = static_cast<char*>(T->data);
+  for (int d = 0; d < T->rank; ++d)
+    if (T->labels[d] == lbl) {
+      lens[(size_t)d] = len;
+      if (base) base += lo * T->strides[d] * (int64_t)esz;
+    }
+  out.lens = lens.data();
+  out.data = base;
+  return out;
+}
+
 int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                 double beta, const tc_tensor* C, void* stream) {
   std::shared_ptr<Plan> p;
@@ -575,6 +592,23 @@ int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tenso
   size_t esz = dtype == TC_F64 ? 8 : 4;
   if (overlaps(A, C, esz) || overlaps(B, C, esz))
     return fail(TC_ERR_ALIAS, "C overlaps A or B");
+  if (p->split_label && alpha != 0.0 && !p->empty_out && p->k > 0 && !force_scatter()) {
+    // sub-division blocked by a length with no small power-of-two divisor (plan.cpp): the
+    // divisible main part of the label (its own plan sub-divides P, or splits again on the
+    // other label), then the remainder accumulated into C
+    std::vector<int64_t> la, lb, lta, ltb;
+    const char x = p->split_label;
+    int64_t len = 0;
+    for (int d = 0; d < A->rank; ++d)
+      if (A->labels[d] == x) len = A->lens[d];
+    const tc_tensor Am = restrict_label(A, x, 0, p->split_main, esz, la);
+    const tc_tensor Bm = restrict_label(B, x, 0, p->split_main, esz, lb);
+    rc = tc_contract(dtype, alpha, &Am, &Bm, beta, C, stream);
+    if (rc != TC_OK || len <= p->split_main) return rc;
+    const tc_tensor At = restrict_label(A, x, p->split_main, len - p->split_main, esz, lta);
+    const tc_tensor Bt = restrict_label(B, x, p->split_main, len - p->split_main, esz, ltb);
+    return tc_contract(dtype, alpha, &At, &Bt, 1.0, C, stream);
+  }
   return execute(*p, alpha, A->data, B->data, beta, C->data, static_cast<cudaStream_t>(stream));
 }
 

@@ -575,6 +575,22 @@ def test_f2_fig_bench_full_sampled(idx):
     assert e < 1e-12
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("lens", [{"a": 40, "b": 36, "c": 67, "d": 130},
+                                  {"a": 33, "b": 50, "c": 67, "d": 71},
+                                  {"a": 130, "b": 129, "c": 323, "d": 66}])
+def test_subdivision_with_remainder(lens, dtype):
+    """fig:bench's ab-cad-dcb class (A and B have different unit-stride dimensions in P) with
+    lengths that have no power-of-two divisor <= 4: the device entry point runs the divisible
+    main part of the label (sub-divided) and the remainder, possibly twice (both labels); beta
+    applies once. Bitwise with integer inputs."""
+    case = W.Case("subrem", "ab", "cad", "dcb", lens, dtype=dtype, alpha=0.5, beta=-0.75,
+                  c_init="dist", seed=61)
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
 @pytest.fixture(params=["1", "0"], ids=["rankk", "tile"])
 def both_rankk_paths(request, monkeypatch):
     """K <= 16 contractions with large free extents through the rank-k kernel (rankk.cu) and,
