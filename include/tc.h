@@ -72,7 +72,10 @@ typedef struct tc_plan tc_plan;
 
 /* C := alpha*A.B + beta*C on DEVICE buffers, asynchronously on `stream`. Plans are cached by
  * (dtype, labels, lens, strides, device), so repeated calls with the same structure skip
- * planning and table upload. */
+ * planning and table upload. When the plan's P sub-division is blocked by a long bound length
+ * with no small power-of-two divisor (R17), the call runs as two or more kernel
+ * launches on `stream`: the divisible main part of that label (with beta), then the remainder
+ * accumulated into C (beta = 1); the result is the same contraction. */
 int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                 double beta, const tc_tensor* C, void* stream);
 
