@@ -103,7 +103,8 @@ int tc_release_staging(void);
 int tc_plan_create(tc_plan** plan, tc_dtype dtype, const tc_tensor* A, const tc_tensor* B,
                    const tc_tensor* C);
 
-/* Execute a plan on device buffers whose structure equals the planned one. */
+/* Execute a plan on device buffers whose structure equals the planned one (one launch, the
+ * plan as built: no remainder split, see tc_contract). */
 int tc_plan_execute(const tc_plan* plan, double alpha, const void* A, const void* B,
                     double beta, void* C, void* stream);
 
