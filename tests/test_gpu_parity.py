@@ -781,23 +781,28 @@ def test_sharded_blocks_assemble_full_result(world):
 # ---------------------------------------------------------------------------------------------
 
 @pytest.mark.usefixtures("both_small_paths")
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
 @pytest.mark.parametrize("lens", [{"m": 128, "n": 128, "k": 160},   # tile kernel, int64 tables
                                   {"m": 5000, "n": 40, "k": 30},    # skinny kernel
-                                  {"m": 20, "n": 12, "k": 30}])     # tiny kernel
-def test_int64_offsets_large_span(lens):
+                                  {"m": 20, "n": 12, "k": 30},      # tiny kernel
+                                  {"m": 2048, "n": 2048, "k": 5}])  # rank-k kernel
+def test_int64_offsets_large_span(lens, dtype):
     """A is a strided view whose K stride is 2^27 elements, so its address span exceeds 2^31
-    elements (a 32 GiB buffer, untouched except where A lives)."""
+    elements (a 16-32 GiB buffer, untouched except where A lives). fp32 takes the FFMA2 tile
+    kernel here (the tcgen05 kernel has 32-bit offsets only)."""
     m, n, k = lens["m"], lens["n"], lens["k"]
     g = torch.Generator().manual_seed(9)
-    A = torch.randint(-4, 5, (m, k), generator=g).double()
-    B = torch.randint(-4, 5, (k, n), generator=g).double()
-    ref = torch.zeros(m, n, dtype=torch.float64)
+    A = torch.randint(-4, 5, (m, k), generator=g).to(dtype)
+    B = torch.randint(-4, 5, (k, n), generator=g).to(dtype)
+    ref = torch.zeros(m, n, dtype=dtype)
     oracle.contract("mn-mk-kn", A, B, ref, 1.0, 0.0)
     stride_k = 1 << 27
-    big = torch.empty(stride_k * (k - 1) + m, dtype=torch.float64, device="cuda")
+    while stride_k * (k - 1) < (1 << 31):   # short K: a longer stride keeps the span > 2^31
+        stride_k *= 2
+    big = torch.empty(stride_k * (k - 1) + m, dtype=dtype, device="cuda")
     Ad = big.as_strided((m, k), (1, stride_k))
     Ad.copy_(A.cuda())
-    Cd = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    Cd = torch.full((m, n), float("nan"), dtype=dtype, device="cuda")
     info = tc().Plan.for_tensors("mn-mk-kn", Ad, B.cuda(), Cd).info()
     assert info["idx64"]
     tc().contract("mn-mk-kn", Ad, B.cuda(), Cd, 1.0, 0.0)
