@@ -687,6 +687,40 @@ def test_guard_bands(seed, dtype):
     assert relerr(got.numpy(), ref.numpy()) <= TOL[dtype]
 
 
+@pytest.mark.parametrize("form", ["128", "256", "pair"])
+@pytest.mark.parametrize("seed", [0, 3, 6, 9])
+def test_guard_bands_f32_forms(seed, form, monkeypatch):
+    """Guard bands for every form of the fp32 tcgen05 kernel on scaled cfg4 cases (several tiles,
+    stream-K pieces, ragged tails)."""
+    monkeypatch.setenv("TC_F32_UMMA", "1")
+    monkeypatch.setenv("TC_UMMA_FORM", form)
+    test_guard_bands(seed, torch.float32)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("spec", ["mn-mk-kn", "nm-km-nk"])
+def test_guard_bands_rankk(spec, dtype):
+    """Guard bands around a rank-k contraction (rankk.cu, both row mappings)."""
+    rs = np.random.RandomState(77)
+    lc, la, lb = spec.split("-")
+    case = W.Case("rkguard", lc, la, lb, {"m": 2050, "n": 2049, "k": 5}, dtype=dtype,
+                  alpha=0.5, beta=0.25, c_init="dist", seed=78)
+    A, B, C = W.make_tensors(case, "cpu")
+    bufA, Ad = _embed(A, "cuda", float("nan"), rs, 2)
+    bufB, Bd = _embed(B, "cuda", float("nan"), rs, 2)
+    bufC, Cd = _embed(C, "cuda", 12345.0, rs, 2)
+    mask = torch.ones(bufC.numel(), dtype=torch.bool, device="cuda")
+    mask.as_strided(Cd.shape, Cd.stride(), Cd.storage_offset()).fill_(False)
+    before = bufC[mask].clone()
+    C0 = Cd.clone()
+    tc().contract(case.spec, Ad, Bd, Cd, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    assert torch.equal(bufC[mask], before), "write outside C"
+    assert torch.isfinite(Cd).all(), "read outside A/B"
+    e, _, _ = sampled_check(case, Ad, Bd, C0, Cd, per_label=8, seed=5)
+    assert e < TOL[dtype]
+
+
 # ---------------------------------------------------------------------------------------------
 # skinny contractions (skinny.cu: fp64, K <= 80, one free extent <= 96, the other >= 4096)
 # ---------------------------------------------------------------------------------------------
