@@ -78,7 +78,8 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 constexpr int kMinSkIters = 8;
 constexpr int kMaxPieces = 16;   // at most this many stream-K pieces per tile (fix-up chain)
 
-inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88) {
+inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88,
+                        int min_sk_iters = kMinSkIters) {
   Sched s{};
   s.T = T; s.KT = KT; s.P = nsm;
   // Which tiles are split: the last full wave and the partial wave (stream-K over 1-2 waves,
@@ -93,7 +94,7 @@ inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88) 
   else D = (T / nsm - 1) * nsm;
   s.D = D;
   s.I = (long long)(T - D) * KT;
-  long long psk = s.I / kMinSkIters;   // each stream-K CTA gets >= kMinSkIters iterations
+  long long psk = s.I / min_sk_iters;   // each stream-K CTA gets >= min_sk_iters iterations
   if (psk < 1) psk = 1;
   if (psk > nsm) psk = nsm;
   if (psk > (long long)(T - D) * kMaxPieces) psk = (long long)(T - D) * kMaxPieces;

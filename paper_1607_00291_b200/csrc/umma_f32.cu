@@ -847,7 +847,11 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   const char* pe = getenv("TC_UMMA_SK");
   const bool sk = a.stream_k && !(pe && !strcmp(pe, "0"));
   const char* pp = getenv("TC_UMMA_DPPCT");   // measurement override of the 70% threshold
-  Sched sc = make_sched(T, KT, units, sk, pp ? atoi(pp) : 70);
+  // stream-K pieces of at least min(KT, 16) K steps (and 8): this kernel's fix-up links are
+  // expensive, so few, longer pieces win on small problems (1024^3: 0.58 -> 0.99 of SGEMM,
+  // 512^3 0.34 -> 0.46; profiles/r01/ab_min_sk.txt)
+  const int min_sk = KT < 8 ? 8 : (KT > 16 ? 16 : KT);
+  Sched sc = make_sched(T, KT, units, sk, pp ? atoi(pp) : 70, min_sk);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, units, false);
   sc.wave_sync = 0;
   const int nunits = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
