@@ -117,6 +117,11 @@ constexpr int kChunkBufs = kN256 ? 1 : (kTmemA ? 2 : 3);
 constexpr int kChunkCols = kN256 ? 2 * BN : BN;
 constexpr int kSumCol = kChunkBufs * kChunkCols;
 constexpr int kACol = kSumCol + BN, kASlots = 2;
+// shared memory: stage ring, barriers, then the epilogue's transpose buffer (32 x 33 floats per
+// epilogue warp) for read-modify-writes of a C whose unit stride runs along N
+constexpr int kBarBytes = (3 * STAGES + 2 * kChunkBufs + kASlots) * 8 + 16;
+constexpr int kEpiOff = (STAGES * kStage * 4 + kBarBytes + 127) / 128 * 128;
+constexpr int kSmemBytes = kEpiOff + 4 * 32 * 33 * 4;
 static_assert(kSumCol + BN + (kTmemA ? kASlots * 2 * BK : 0) <= 512, "TMEM columns");
 
 __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u32(p); }
@@ -342,6 +347,29 @@ __device__ __forceinline__ void epi_sync() {   // the four epilogue warps only
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
 }
 
+// Read-modify-write of one 32 x 32 block of C (32 rows of this warp, 32 columns) when C's unit
+// stride runs along N: the block is staged transposed in shared memory (stg, written by the
+// caller as [row][col], pitch 33), so each warp load / store covers 32 consecutive columns of
+// one row instead of 32 rows. Out of line, so its registers stay out of the kernel's loops.
+template <typename IDX>
+__device__ __noinline__ void rmw_block_transposed(const float* stg, float* C, IDX rc, IDX col,
+                                                  int mrow0, int M, bool cin, int piece,
+                                                  double alpha, double beta, int lane) {
+  float old[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const IDX rr = __shfl_sync(0xffffffffu, rc, r);
+    old[r] = (cin && mrow0 + r < M) ? C[rr + col] : 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const IDX rr = __shfl_sync(0xffffffffu, rc, r);
+    double out = alpha * static_cast<double>(stg[r * 33 + lane]);
+    out = piece > 0 ? out + static_cast<double>(old[r]) : fma(beta, static_cast<double>(old[r]), out);
+    if (cin && mrow0 + r < M) C[rr + col] = static_cast<float>(out);
+  }
+}
+
 // cluster (CTA pair) helpers
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -382,7 +410,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
                    const IDX* __restrict__ rB, const IDX* __restrict__ cB,
                    const IDX* __restrict__ rC, const IDX* __restrict__ cC, int M, int N, int K,
                    int tiles_m, int tiles_n, double alpha, double beta, Sched sched,
-                   int* __restrict__ flags) {
+                   int* __restrict__ flags, bool c_lanes_n) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* stage0 = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * kStage * sizeof(float));
@@ -392,6 +420,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   uint64_t* tempty = tfull + kChunkBufs;
   uint64_t* aempty = tempty + kChunkBufs;   // [kASlots] (A in TMEM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + kASlots);
+  float* epi_stage = reinterpret_cast<float*>(smem_raw + kEpiOff);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef TC_UMMA_PROF
@@ -662,7 +691,15 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
             const bool full = nb + 32 <= N;
             const IDX col = c0 == 0 ? colv[0] : c0 == 1 ? colv[1] : c0 == 2 ? colv[2] : colv[3];
             // (no branch on the row: the shuffles need the whole warp)
-            if (read_c) {
+            if (read_c && c_lanes_n) {
+              float* stg = epi_stage + q * 32 * 33;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(u[i]);
+              __syncwarp();
+              rmw_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, piece, alpha,
+                                        beta, lane);
+              __syncwarp();
+            } else if (read_c) {
               float old[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
@@ -832,8 +869,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 
 template <typename IDX, int A_MODE, int B_MODE>
 static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
-  constexpr int smem =
-      STAGES * kStage * (int)sizeof(float) + (3 * STAGES + 2 * kChunkBufs + kASlots) * 8 + 16;
+  constexpr int smem = kSmemBytes;
   auto kern = tc_umma_f32_kernel<IDX, A_MODE, B_MODE>;
   static std::atomic<int> attr[kMaxDevices];
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
@@ -875,11 +911,13 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
     cfg.attrs = attr1;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, kern, pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
-                           tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags) != cudaSuccess)
+                           tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags, a.c_lanes_n) !=
+        cudaSuccess)
       return -1;
   } else {
     kern<<<nunits, kThreads, smem, s>>>(pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
-                                        tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags);
+                                        tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags,
+                                        a.c_lanes_n);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
