@@ -370,6 +370,23 @@ __device__ __noinline__ void rmw_block_transposed(const float* stg, float* C, ID
   }
 }
 
+// Write-only counterpart (TC_UMMA_WT=1: measurement switch): alpha * block through the same
+// transpose, one 128-byte row segment per warp store.
+#ifndef TC_UMMA_WT
+#define TC_UMMA_WT 0
+#endif
+template <typename IDX>
+__device__ __noinline__ void store_block_transposed(const float* stg, float* C, IDX rc, IDX col,
+                                                    int mrow0, int M, bool cin, double alpha,
+                                                    int lane) {
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const IDX rr = __shfl_sync(0xffffffffu, rc, r);
+    if (cin && mrow0 + r < M)
+      C[rr + col] = static_cast<float>(alpha * static_cast<double>(stg[r * 33 + lane]));
+  }
+}
+
 // cluster (CTA pair) helpers
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -698,6 +715,13 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               __syncwarp();
               rmw_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, piece, alpha,
                                         beta, lane);
+              __syncwarp();
+            } else if (TC_UMMA_WT && !read_c && c_lanes_n) {
+              float* stg = epi_stage + q * 32 * 33;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(u[i]);
+              __syncwarp();
+              store_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, alpha, lane);
               __syncwarp();
             } else if (read_c) {
               float old[32];
