@@ -1015,7 +1015,10 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
     const char* e = getenv("TC_WS_DPPCT");
     return e ? atoi(e) : 88;
   }();
-  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k, dp_pct);
+  // up to 48 stream-K pieces per tile: few-tile, long-K shapes then keep every SM busy (this
+  // kernel's fix-up links are cheap: 256^2 x 65536 0.39 -> 0.52, 128^2 x 262144 0.12 -> 0.27 of
+  // DGEMM; profiles/r01/ab_max_pieces.txt)
+  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k, dp_pct, kMinSkIters, 48);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) {   // cannot happen: S < 2 * num_sms
     Sched dp = make_sched(tiles_m * tiles_n, KT, a.num_sms, false);
     sc = dp;

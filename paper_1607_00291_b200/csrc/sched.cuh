@@ -79,7 +79,7 @@ constexpr int kMinSkIters = 8;
 constexpr int kMaxPieces = 16;   // at most this many stream-K pieces per tile (fix-up chain)
 
 inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88,
-                        int min_sk_iters = kMinSkIters) {
+                        int min_sk_iters = kMinSkIters, int max_pieces = kMaxPieces) {
   Sched s{};
   s.T = T; s.KT = KT; s.P = nsm;
   // Which tiles are split: the last full wave and the partial wave (stream-K over 1-2 waves,
@@ -97,7 +97,7 @@ inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88,
   long long psk = s.I / min_sk_iters;   // each stream-K CTA gets >= min_sk_iters iterations
   if (psk < 1) psk = 1;
   if (psk > nsm) psk = nsm;
-  if (psk > (long long)(T - D) * kMaxPieces) psk = (long long)(T - D) * kMaxPieces;
+  if (psk > (long long)(T - D) * max_pieces) psk = (long long)(T - D) * max_pieces;
   s.P_sk = D < T ? (int)psk : 0;
   return s;
 }
