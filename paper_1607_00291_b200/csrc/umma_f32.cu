@@ -459,7 +459,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], kPW * 32);
-      mbar_init(&conv[s], (kPair ? 2 : 1) * kCW * 32);   // pair: both CTAs' converters
+      mbar_init(&conv[s], (kPair ? 2 : 1) * kCW);   // one arrival per converter warp
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < kChunkBufs; ++a) {
@@ -605,8 +605,11 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // visible to the MMA
-        if constexpr (kPair) mbar_arrive_remote(&conv[s], 0);   // the leader's barrier
-        else mbar_arrive(&conv[s]);
+        __syncwarp();   // every lane has fenced its writes; one arrival per warp
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_remote(&conv[s], 0);   // the leader's barrier
+          else mbar_arrive(&conv[s]);
+        }
       }
     }
   } else if (warp < kMmaW) {
