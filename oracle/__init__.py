@@ -6,6 +6,10 @@ and bench.py's cpu_baseline / `--impl reference` leg may import it; the product 
 
   contract(spec, A, B, C, alpha, beta)      plain C nested loops (oracle/contract.c), in place on C
   contract_at(spec, A, B, C, alpha, beta, idx)  the same definition for selected C elements only
+  freivalds(spec, A, B, C_new, C_old, x)    pin p8: the matrix-form products B·x, A·(B·x), C_new·x,
+                                            C_old·x for a full-tensor check of results too large
+                                            for contract() (plain C loops, oracle/contract.c)
+  freivalds_check(...)                      p8's exact (integer inputs) or normwise residual test
   brute(spec, A, B, C, alpha, beta)         a second, pure-Python statement (itertools over a dict
                                             of label values) used to pin contract() on tiny inputs
   plan.*                                    the integer steps a1-a4 (classification, heuristic,
@@ -64,6 +68,15 @@ def _load():
                                                   ctypes.POINTER(ctypes.c_double), ctypes.c_int]
         lib.oracle_contract_at.restype = ctypes.c_int
         lib.oracle_max_threads.restype = ctypes.c_int
+        targs = []
+        for _ in range(3):
+            targs += [ctypes.c_void_p, ctypes.c_int, I64P, I64P, ctypes.c_char_p]
+        lib.oracle_freivalds_dims.argtypes = [a for a in targs if a is not ctypes.c_void_p] + [I64P]
+        lib.oracle_freivalds_dims.restype = ctypes.c_int
+        DP = ctypes.POINTER(ctypes.c_double)
+        lib.oracle_freivalds.argtypes = [ctypes.c_int] + targs + [ctypes.c_void_p, I64P] + \
+            [DP] * 5 + [ctypes.c_int]
+        lib.oracle_freivalds.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -93,7 +106,7 @@ def _arr(xs):
     return a
 
 
-ERRORS = {1: "rank too large", 2: "label error", 3: "shape error"}
+ERRORS = {1: "rank too large", 2: "label error", 3: "shape error", 4: "out of host memory"}
 
 
 def _parse(spec: str):
@@ -173,3 +186,87 @@ def flops(spec: str, lens: dict) -> int:
     for x in set(lab_a) | set(lab_b) | set(lab_c):
         n *= lens[x]
     return 2 * n
+
+
+def freivalds_dims(spec: str, A, B, C):
+    """(n_I, n_J, n_P): extents of the I = C∩A, J = C∩B, P = A∩B label groups."""
+    (a, b, c), _code, _keep = _args(spec, A, B, C)
+    dims = (ctypes.c_int64 * 3)()
+    err = _load().oracle_freivalds_dims(*a[1:], *b[1:], *c[1:], dims)
+    if err:
+        raise ValueError(f"oracle: {ERRORS.get(err, err)} for {spec!r}")
+    return int(dims[0]), int(dims[1]), int(dims[2])
+
+
+def freivalds(spec: str, A, B, C_new, C_old, x: np.ndarray, threads: Optional[int] = None):
+    """Pin p8: the matrix-form products of oracle/contract.c's
+    oracle_freivalds for one vector x over J (colexicographic over the J labels in C's order).
+    Returns dict(u=B·x [n_P], v=A·u [n_I], wnew=C_new·x [n_I], wold=C_old·x [n_I] or None).
+    C_old may be None (beta == 0: C_old is not read)."""
+    (a, b, c), code, _keep = _args(spec, A, B, C_new)
+    nI, nJ, nP = freivalds_dims(spec, A, B, C_new)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    assert x.shape == (nJ,), (x.shape, nJ)
+    sold, pold, keep2 = None, None, None
+    if C_old is not None:
+        p, lens, strides, code2 = _view(C_old)
+        if code2 != code or lens != list(_view(C_new)[1]):
+            raise ValueError("C_old must match C_new's dtype and shape")
+        keep2 = _arr(strides)
+        sold, pold = keep2, ctypes.c_void_p(p)
+    u = np.zeros(max(nP, 1)); v = np.zeros(max(nI, 1))
+    wn = np.zeros(max(nI, 1)); wo = np.zeros(max(nI, 1))
+    DP = ctypes.POINTER(ctypes.c_double)
+    err = _load().oracle_freivalds(code, *a, *b, *c, pold, sold,
+                                   x.ctypes.data_as(DP), u.ctypes.data_as(DP),
+                                   v.ctypes.data_as(DP), wn.ctypes.data_as(DP),
+                                   wo.ctypes.data_as(DP), int(threads or 0))
+    if err:
+        raise ValueError(f"oracle: {ERRORS.get(err, err)} for {spec!r}")
+    return dict(u=u[:nP], v=v[:nI], wnew=wn[:nI], wold=wo[:nI] if C_old is not None else None)
+
+
+def freivalds_vectors(nJ: int, nvec: int = 3, seed: int = 0, lo: int = -1024, hi: int = 1024):
+    """Seeded integer test vectors x in [lo, hi]^nJ, float64."""
+    rs = np.random.RandomState(seed)
+    return [rs.randint(lo, hi + 1, size=nJ).astype(np.float64) for _ in range(nvec)]
+
+
+def frob(T) -> float:
+    """Frobenius norm of a tensor's elements (the norm of its matrix form)."""
+    try:
+        import torch
+        if isinstance(T, torch.Tensor):
+            return float(torch.linalg.vector_norm(T.double() if T.dtype != torch.float64 else T))
+    except ImportError:  # pragma: no cover
+        pass
+    return float(np.linalg.norm(np.asarray(T, dtype=np.float64).ravel()))
+
+
+def freivalds_check(spec: str, A, B, C_new, C_old, alpha: float, beta: float, nvec: int = 3,
+                    seed: int = 0, exact: bool = False, threads: Optional[int] = None):
+    """Pin p8: for nvec seeded x, compare C_new·x with alpha·A·(B·x) + beta·C_old·x.
+    exact=True (integer inputs, every partial sum exact): bitwise equality, returns 0.0 or the
+    largest |difference|. Otherwise the normwise residual
+      ||C_new·x − alpha·A·(B·x) − beta·C_old·x|| / (|alpha|·||A||_F·||B·x|| + |beta|·||C_old·x||)
+    maximised over the vectors."""
+    nI, nJ, nP = freivalds_dims(spec, A, B, C_new)
+    worst = 0.0
+    normA = None
+    for x in freivalds_vectors(nJ, nvec, seed):
+        r = freivalds(spec, A, B, C_new, C_old if beta != 0.0 else None, x, threads)
+        rhs = alpha * r["v"]
+        if beta != 0.0:
+            rhs = rhs + beta * r["wold"]
+        d = r["wnew"] - rhs
+        if exact:
+            worst = max(worst, float(np.abs(d).max()) if d.size else 0.0)
+            continue
+        if normA is None:
+            normA = frob(A)
+        den = abs(alpha) * normA * float(np.linalg.norm(r["u"]))
+        if beta != 0.0:
+            den += abs(beta) * float(np.linalg.norm(r["wold"]))
+        num = float(np.linalg.norm(d))
+        worst = max(worst, num / den if den > 0 else num)
+    return worst

@@ -197,3 +197,164 @@ int oracle_contract_at(int dtype, double alpha,
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Pin p8: Freivalds' full-tensor check, for results the element-wise
+ * definition above cannot finish at full size (cfg3, cfg5, each multi-GPU shard).
+ *
+ * View the contraction in its matrix form (§3, §6.1: every free index of
+ * C is a pair (I, J), every element of A a pair (I, P), of B a pair (P, J)):
+ *     C_new = alpha * A B + beta * C_old.
+ * Multiplying both sides by a vector x over J (colexicographic over the J labels in C's label
+ * order, the first fastest, as P:528-529) gives, for every I,
+ *     sum_J C_new[I,J] x[J]  ==  alpha * sum_P A[I,P] * (sum_J B[P,J] x[J])
+ *                                + beta * sum_J C_old[I,J] x[J].
+ * A wrong C_new[I,J] changes the left side at I by (error * x[J]); Freivalds (1977).
+ *
+ * Groups: I = labels of C that are in A (C's order), J = labels of C that are in B (C's order),
+ * P = labels of A not in C (A's order). Every location is loc = sum_x idx_x * stride_x
+ * (P:569-571); the sum over a label group splits into the I, J, P parts, and each part is
+ * tabulated once per group (offI/offJ/offP below) -- only the associativity of that sum.
+ *
+ * Outputs (all double, the caller owns them):
+ *   u[nP]    = sum_J B[P,J] x[J]
+ *   v[nI]    = sum_P A[I,P] u[P]
+ *   wnew[nI] = sum_J C_new[I,J] x[J]
+ *   wold[nI] = sum_J C_old[I,J] x[J]   (not computed, left untouched, when Cold == NULL)
+ * Each output element is summed in ascending order of its summation index. The loops over the
+ * output index are grouped in blocks of FV_BLK consecutive outputs so that consecutive output
+ * elements read neighbouring memory; this changes no value (each output keeps its own
+ * accumulator and its own ascending summation order).
+ * Returns 0 or the same error codes as oracle_contract.
+ * ---------------------------------------------------------------------------------------- */
+
+#define FV_BLK 64
+
+typedef struct {
+  int n;
+  int64_t len[OR_MAXR];
+  int64_t s1[OR_MAXR];       /* stride in the first tensor carrying the group */
+  int64_t s2[OR_MAXR];       /* stride in the second tensor carrying the group */
+} fv_group;
+
+/* I = C∩A (C order), J = C∩B (C order), P = A∩B (A order), after the same label checks as
+ * classify(). For I: s1 = stride in A, s2 = stride in C. J: s1 = B, s2 = C. P: s1 = A, s2 = B. */
+static int fv_classify(int rA, const int64_t* lA, const int64_t* sA, const char* labA,
+                       int rB, const int64_t* lB, const int64_t* sB, const char* labB,
+                       int rC, const int64_t* lC, const int64_t* sC, const char* labC,
+                       fv_group* I, fv_group* J, fv_group* P) {
+  or_group F, Q;
+  int err = classify(rA, lA, sA, labA, rB, lB, sB, labB, rC, lC, sC, labC, &F, &Q);
+  if (err) return err;
+  I->n = J->n = P->n = 0;
+  for (int i = 0; i < rC; ++i) {
+    int ia = find(labA, rA, labC[i]);
+    if (ia >= 0) {
+      I->len[I->n] = lC[i]; I->s1[I->n] = sA[ia]; I->s2[I->n] = sC[i]; I->n++;
+    } else {
+      int ib = find(labB, rB, labC[i]);
+      J->len[J->n] = lC[i]; J->s1[J->n] = sB[ib]; J->s2[J->n] = sC[i]; J->n++;
+    }
+  }
+  for (int i = 0; i < Q.n; ++i) {
+    P->len[i] = Q.len[i]; P->s1[i] = Q.sa[i]; P->s2[i] = Q.sb[i];
+  }
+  P->n = Q.n;
+  return 0;
+}
+
+static int64_t fv_extent(const fv_group* g) {
+  int64_t n = 1;
+  for (int i = 0; i < g->n; ++i) n *= g->len[i];
+  return n;
+}
+
+/* off1[q], off2[q]: location part of group g at linear index q (colexicographic, first fastest),
+ * in the first and second tensor carrying g. */
+static void fv_offsets(const fv_group* g, int64_t n, int64_t* off1, int64_t* off2) {
+  for (int64_t q = 0; q < n; ++q) {
+    int64_t r = q, o1 = 0, o2 = 0;
+    for (int i = 0; i < g->n; ++i) {
+      int64_t x = r % g->len[i];
+      r /= g->len[i];
+      o1 += x * g->s1[i]; o2 += x * g->s2[i];
+    }
+    off1[q] = o1; off2[q] = o2;
+  }
+}
+
+static double fv_load(int dtype, const void* T, int64_t loc) {
+  return dtype == 0 ? ((const double*)T)[loc] : (double)((const float*)T)[loc];
+}
+
+/* y[r] = sum_{q=0}^{nQ-1} T[offR[r] + offQ[q]] * z[q], for r in [0, nR). */
+static void fv_matvec(int dtype, const void* T, const int64_t* offR, int64_t nR,
+                      const int64_t* offQ, int64_t nQ, const double* z, double* y) {
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t r0 = 0; r0 < nR; r0 += FV_BLK) {
+    int64_t r1 = r0 + FV_BLK < nR ? r0 + FV_BLK : nR;
+    double acc[FV_BLK];
+    for (int64_t r = r0; r < r1; ++r) acc[r - r0] = 0.0;
+    for (int64_t q = 0; q < nQ; ++q) {
+      double zq = z[q];
+      int64_t oq = offQ[q];
+      for (int64_t r = r0; r < r1; ++r) acc[r - r0] += fv_load(dtype, T, offR[r] + oq) * zq;
+    }
+    for (int64_t r = r0; r < r1; ++r) y[r] = acc[r - r0];
+  }
+}
+
+/* Group extents (nI, nJ, nP) of a contraction, for sizing the Freivalds vectors. */
+int oracle_freivalds_dims(int rA, const int64_t* lA, const int64_t* sA, const char* labA,
+                          int rB, const int64_t* lB, const int64_t* sB, const char* labB,
+                          int rC, const int64_t* lC, const int64_t* sC, const char* labC,
+                          int64_t* dims) {
+  fv_group I, J, P;
+  int err = fv_classify(rA, lA, sA, labA, rB, lB, sB, labB, rC, lC, sC, labC, &I, &J, &P);
+  if (err) return err;
+  dims[0] = fv_extent(&I); dims[1] = fv_extent(&J); dims[2] = fv_extent(&P);
+  return 0;
+}
+
+/* C_new and C_old carry the same labels and lengths (strides may differ: sCold). */
+int oracle_freivalds(int dtype,
+                     const void* A, int rA, const int64_t* lA, const int64_t* sA, const char* labA,
+                     const void* B, int rB, const int64_t* lB, const int64_t* sB, const char* labB,
+                     const void* Cnew, int rC, const int64_t* lC, const int64_t* sC, const char* labC,
+                     const void* Cold, const int64_t* sCold,
+                     const double* x, double* u, double* v, double* wnew, double* wold,
+                     int nthreads) {
+  fv_group I, J, P;
+  int err = fv_classify(rA, lA, sA, labA, rB, lB, sB, labB, rC, lC, sC, labC, &I, &J, &P);
+  if (err) return err;
+  int64_t nI = fv_extent(&I), nJ = fv_extent(&J), nP = fv_extent(&P);
+  int64_t* oIA = malloc(sizeof(int64_t) * (nI ? nI : 1));
+  int64_t* oIC = malloc(sizeof(int64_t) * (nI ? nI : 1));
+  int64_t* oJB = malloc(sizeof(int64_t) * (nJ ? nJ : 1));
+  int64_t* oJC = malloc(sizeof(int64_t) * (nJ ? nJ : 1));
+  int64_t* oPA = malloc(sizeof(int64_t) * (nP ? nP : 1));
+  int64_t* oPB = malloc(sizeof(int64_t) * (nP ? nP : 1));
+  if (!oIA || !oIC || !oJB || !oJC || !oPA || !oPB) {
+    free(oIA); free(oIC); free(oJB); free(oJC); free(oPA); free(oPB);
+    return 4;
+  }
+  fv_offsets(&I, nI, oIA, oIC);
+  fv_offsets(&J, nJ, oJB, oJC);
+  fv_offsets(&P, nP, oPA, oPB);
+  set_threads(nthreads);
+  fv_matvec(dtype, B, oPB, nP, oJB, nJ, x, u);          /* u = B x      */
+  fv_matvec(dtype, A, oIA, nI, oPA, nP, u, v);          /* v = A u      */
+  fv_matvec(dtype, Cnew, oIC, nI, oJC, nJ, x, wnew);    /* wnew = Cnew x */
+  if (Cold) {                                           /* wold = Cold x */
+    fv_group Jo = J, Io = I;
+    for (int i = 0, a = 0, b = 0; i < rC; ++i) {        /* C_old's own strides, same labels */
+      if (find(labA, rA, labC[i]) >= 0) Io.s2[a++] = sCold[i];
+      else Jo.s2[b++] = sCold[i];
+    }
+    fv_offsets(&Io, nI, oIA, oIC);
+    fv_offsets(&Jo, nJ, oJB, oJC);
+    fv_matvec(dtype, Cold, oIC, nI, oJC, nJ, x, wold);
+  }
+  free(oIA); free(oIC); free(oJB); free(oJC); free(oPA); free(oPB);
+  return 0;
+}
