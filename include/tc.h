@@ -104,7 +104,11 @@ int tc_plan_create(tc_plan** plan, tc_dtype dtype, const tc_tensor* A, const tc_
                    const tc_tensor* C);
 
 /* Execute a plan on device buffers whose structure equals the planned one (one launch, the
- * plan as built: no remainder split, see tc_contract). */
+ * plan as built: no remainder split, see tc_contract -- the result is the same, only the
+ * R17 speed-up of labels without a small power-of-two divisor is missing). The data pointers
+ * are checked like tc_contract's: TC_ERR_ARG if misaligned or NULL where read, TC_ERR_ALIAS if
+ * C's address span (from the planned lengths and strides) overlaps A's or B's; nothing is
+ * enqueued then. */
 int tc_plan_execute(const tc_plan* plan, double alpha, const void* A, const void* B,
                     double beta, void* C, void* stream);
 

@@ -191,12 +191,18 @@ def contract(spec: str, A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=N
                            ctypes.byref(dB.t), ctypes.byref(dC.t), (dA, dB, dC))
     if not (A.is_cuda and B.is_cuda and C.is_cuda):
         raise ValueError("contract() takes CUDA tensors; use contract_host() for host memory")
+    if A.dtype is not C.dtype or B.dtype is not C.dtype:
+        raise TypeError(f"A, B, C must share one dtype (got {A.dtype}, {B.dtype}, {C.dtype})")
+    dev = torch_C._cuda_getDevice()
+    if A.get_device() != dev or B.get_device() != dev or C.get_device() != dev:
+        raise ValueError(f"A, B, C must be on the current CUDA device (cuda:{dev}); got "
+                         f"{A.device}, {B.device}, {C.device}")
     code, tA, tB, tC, pA, pB, pC, _ = ent
     tA.data = A.data_ptr()
     tB.data = B.data_ptr()
     tC.data = C.data_ptr()
     if stream is None:
-        sp = torch_C._cuda_getCurrentRawStream(torch_C._cuda_getDevice())
+        sp = torch_C._cuda_getCurrentRawStream(dev)
     else:
         sp = stream.cuda_stream
     rc = _lib.tc_contract(code, alpha, pA, pB, beta, pC, sp)
@@ -209,6 +215,10 @@ def contract_host(spec: str, A, B, C, alpha: float = 1.0, beta: float = 0.0, str
     """End-to-end path on host tensors (pinned for full bandwidth): the library copies the
     operands to the current CUDA device, contracts, and copies C back (synchronous)."""
     lc, la, lb = parse_spec(spec)
+    if A.dtype is not C.dtype or B.dtype is not C.dtype:
+        raise TypeError(f"A, B, C must share one dtype (got {A.dtype}, {B.dtype}, {C.dtype})")
+    if A.is_cuda or B.is_cuda or C.is_cuda:
+        raise ValueError("contract_host() takes host tensors; use contract() for CUDA tensors")
     tc_contract_host(_dtype_code(C.dtype), alpha, _desc(A, la, 0), _desc(B, lb, 1), beta,
                      _desc(C, lc, 2), _stream_ptr(stream))
     return C
@@ -238,6 +248,8 @@ class Plan:
             self._p = ctypes.c_void_p()
 
     def execute(self, A, B, C, alpha: float = 1.0, beta: float = 0.0, stream=None):
+        if A.dtype is not C.dtype or B.dtype is not C.dtype:
+            raise TypeError("A, B, C must share one dtype")
         _check(_lib.tc_plan_execute(self._p, float(alpha), A.data_ptr(), B.data_ptr(),
                                     float(beta), C.data_ptr(), _stream_ptr(stream)))
         return C

@@ -425,7 +425,7 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
     if (r != 0) return r;
   }
   LaunchArgs a = args;
-  a.stream_k = choice != 2;
+  a.stream_k = args.stream_k && choice != 2;
   return launch_ws(a, stream);
 }
 

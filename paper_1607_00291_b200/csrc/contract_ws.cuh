@@ -775,8 +775,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       piece = blockIdx.x - owner;
       flag = flags + s_local;
       if (piece > 0) {
-        if (threadIdx.x == 0)
-          while (ld_acquire(flag) != piece) __nanosleep(100);
+        if (threadIdx.x == 0) wait_flag(flag, (int)(sched.epoch | (unsigned)piece));
         consumers_sync();
       }
     }
@@ -990,12 +989,11 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     }
     }   // DMMA epilogue
     if (split) {
-      // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
-      // again when the kernel ends (no per-launch reset)
+      // publish this piece (epoch-tagged: nothing is reset for the next launch)
       consumers_sync();
       if (threadIdx.x == 0) {
         __threadfence();
-        st_release(flag, ke < sched.KT ? piece + 1 : 0);
+        if (ke < sched.KT) st_release(flag, (int)(sched.epoch | (unsigned)(piece + 1)));
       }
     }
   }
@@ -1024,13 +1022,14 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
     sc = dp;
   }
   int* flags = a.flags;
+  sc.epoch = a.flag_epoch;
   const int grid = sc.D > 0 ? sc.P : sc.P_sk;
   // wave alignment only pays when a tile's K panels are long enough for L2 sharing to matter;
   // with short K loops the per-wave wait is pure overhead (f1 k5: 15% of samples at the barrier)
   sc.wave_sync = a.wave_sync && a.wave_base != nullptr && sc.D >= 2 * sc.P && KT >= 64;
   if (sc.wave_sync) {
-    sc.wave_base = *a.wave_base;
-    *a.wave_base += (unsigned)sc.D;   // every whole tile adds one to the counter
+    // every whole tile adds one to the device counter
+    sc.wave_base = a.wave_base->fetch_add((unsigned)sc.D, std::memory_order_relaxed);
   }
   kern<<<grid, NTHREADS, smem, stream>>>(
       static_cast<const T*>(a.A), static_cast<const T*>(a.B), static_cast<T*>(a.C),

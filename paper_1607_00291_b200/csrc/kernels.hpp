@@ -41,9 +41,12 @@ struct LaunchArgs {
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA
-  int* flags;         // stream-K fix-up flags: >= flags_cap zeroed ints, private to the stream
+  int* flags;         // stream-K fix-up flags: >= flags_cap ints, private to the stream
   int flags_cap;      // flags[flags_cap] is the wave counter (monotonic, see Sched)
-  unsigned* wave_base;   // host copy of the wave counter's value for this stream
+  // host copy of the stream's wave counter: a launch that aligns its waves takes its start
+  // value and adds its whole tiles atomically (concurrent host threads on one stream)
+  std::atomic<unsigned>* wave_base;
+  unsigned flag_epoch;   // this launch's flag epoch, already shifted (epoch << 8, epoch >= 1)
   bool wave_sync;
 };
 

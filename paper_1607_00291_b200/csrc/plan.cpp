@@ -223,6 +223,7 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
   if (!injective(C.rank, C.lens, C.strides))
     return Status::err(TC_ERR_ALIAS, "C is not injective (two index tuples share an address)");
   p->dtype = dtype;
+  for (int t = 0; t < 3; ++t) span(T[t]->rank, T[t]->lens, T[t]->strides, &p->span_lo[t], &p->span_hi[t]);
   p->empty_out = false;
   for (int i = 0; i < C.rank; ++i)
     if (C.lens[i] == 0) p->empty_out = true;

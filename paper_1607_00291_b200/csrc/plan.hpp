@@ -87,6 +87,9 @@ struct Plan {
   char split_label = 0;
   int64_t split_main = 0;
   int variant = 0;
+  // element-offset spans [lo, hi] of A, B, C (caller's roles, before any swap): the alias
+  // check of tc_plan_execute, which gets bare data pointers
+  int64_t span_lo[3] = {1, 1, 1}, span_hi[3] = {0, 0, 0};
   // per-device uploaded tables
   mutable std::mutex mu;
   mutable std::vector<DeviceTables*> dev;

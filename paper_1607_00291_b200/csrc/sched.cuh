@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 #include <cuda_runtime.h>
 
@@ -30,6 +31,10 @@ struct Sched {
   // and B panels in L2 instead of drifting apart over hundreds of waves
   unsigned wave_base;
   int wave_sync;
+  // stream-K flags carry this launch's epoch in their upper 24 bits (epoch << 8) and a piece
+  // count in the low 8 bits: a value left behind by any earlier launch on the stream, finished
+  // or aborted, never matches, so no per-launch reset is needed and none can be missed
+  unsigned epoch;
 };
 
 struct WorkIter {
@@ -70,6 +75,40 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// Wait until a stream-K flag holds `target` (epoch | piece). A piece only waits for lower-ranked
+// CTAs' first work items, so the wait is bounded by one piece's run time; past kFlagTimeoutNs
+// something is broken (a CTA that never ran, corrupted flags) and the kernel traps instead of
+// spinning forever: the launch fails with cudaErrorLaunchFailure / an illegal-instruction error.
+constexpr unsigned long long kFlagTimeoutNs = 30ull * 1000000000ull;
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+static __device__ __noinline__ void flag_timeout(const int* flag, int target) {
+  printf("tc_b200: stream-K fix-up flag timeout (block %d, flag %d, want %d)\n",
+         (int)blockIdx.x, ld_acquire(flag), target);
+  __trap();
+}
+__device__ __forceinline__ void wait_flag(const int* flag, int target) {
+  if (ld_acquire(flag) == target) return;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire(flag) != target) {
+    __nanosleep(64);
+    if (global_ns() - t0 > kFlagTimeoutNs) flag_timeout(flag, target);
+  }
+}
+// Count one arrival on a flag of this launch's epoch: a value from another epoch counts as 0.
+__device__ __forceinline__ void count_flag(int* flag, unsigned epoch) {
+  int old = ld_acquire(flag);
+  while (true) {
+    const int nw = ((unsigned)old & ~0xffu) == epoch ? old + 1 : (int)(epoch | 1u);
+    const int prev = atomicCAS(flag, old, nw);
+    if (prev == old) break;
+    old = prev;
+  }
 }
 
 // Host side of the schedule: D whole tiles round-robin over P = #SMs CTAs, the rest split by

@@ -1,5 +1,6 @@
 // C ABI (include/tc.h): validation, plan cache, device tables, host (end-to-end) path.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -35,6 +36,7 @@ struct DeviceTables {
   void* tab[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint8_t* vA = nullptr;
   uint8_t* vB = nullptr;
+  uint8_t* vZ = nullptr;   // all-zero flags as long as vA and vB (TC_FORCE_PATH=scatter)
   ~DeviceTables() {
     int cur = -1;
     cudaGetDevice(&cur);
@@ -42,13 +44,15 @@ struct DeviceTables {
     for (auto& p : tab) cudaFree(p);
     cudaFree(vA);
     cudaFree(vB);
+    cudaFree(vZ);
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
 
-// Stream-K fix-up flags, one zeroed buffer of 2 * #SMs ints per (device, stream). The kernel
-// leaves every flag at 0 when it ends, so a buffer is reused without a reset; launches on one
-// stream are ordered, launches on different streams use different buffers.
+// Stream-K fix-up flags, one buffer of 2 * #SMs ints per (device, stream). Every launch tags its
+// flag values with a fresh epoch (sched.cuh), so a buffer is reused without a reset and a launch
+// that was aborted half-way cannot poison later ones; launches on one stream are ordered,
+// launches on different streams use different buffers.
 struct FlagKey {
   int device;
   cudaStream_t stream;
@@ -60,7 +64,8 @@ struct FlagKey {
 // whole tile adds 1) and the host keeps its expected value per stream (`wave_base`).
 struct StreamFlags {
   int* flags = nullptr;
-  unsigned wave_base = 0;
+  std::atomic<unsigned> wave_base{0};
+  std::atomic<unsigned> epoch{0};   // stream-K flag epochs handed out (sched.cuh)
 };
 static std::mutex g_flags_mu;
 static std::map<FlagKey, StreamFlags> g_flags;
@@ -72,7 +77,13 @@ static StreamFlags* stream_flags(int device, cudaStream_t s, int cap) {
   int* f = nullptr;
   if (cudaMalloc(reinterpret_cast<void**>(&f), sizeof(int) * (size_t)(cap + 1)) != cudaSuccess)
     return nullptr;
-  if (cudaMemset(f, 0, sizeof(int) * (size_t)(cap + 1)) != cudaSuccess) { cudaFree(f); return nullptr; }
+  // zeroed on the legacy stream, then waited for: the first launch may come on any stream,
+  // including a non-blocking one that is not ordered after the legacy stream
+  if (cudaMemset(f, 0, sizeof(int) * (size_t)(cap + 1)) != cudaSuccess ||
+      cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess) {
+    cudaFree(f);
+    return nullptr;
+  }
   StreamFlags& sf = g_flags[{device, s}];
   sf.flags = f;
   return &sf;
@@ -121,37 +132,37 @@ static cudaError_t upload_bytes(const std::vector<uint8_t>& v, uint8_t** out) {
   return cudaMemcpy(*out, v.data(), v.size(), cudaMemcpyHostToDevice);
 }
 
+// The switches below are read on every call (a getenv per call costs well under a microsecond),
+// so tests and ablations can flip them within one process.
+//
 // TC_FORCE_PATH=scatter: ablation of the block-scatter fast paths (the paper's SMTC):
 // every vector flag is 0 and no operand is treated as vectorisable, so every element is an
-// individual gather through the scatter vectors.
-static bool force_scatter() {
-  static const bool f = [] {
-    const char* e = getenv("TC_FORCE_PATH");
-    return e && !strcmp(e, "scatter");
-  }();
-  return f;
+// individual gather through the scatter vectors. TC_FORCE_PATH=blockscatter: every operand that
+// is not proven all-vector takes the per-vector block-scatter check (gather mode 1)
+// instead of the plan's choice.
+static int force_path() {
+  const char* e = getenv("TC_FORCE_PATH");
+  if (e && !strcmp(e, "scatter")) return 1;
+  if (e && !strcmp(e, "blockscatter")) return 2;
+  return 0;
 }
+static bool force_scatter() { return force_path() == 1; }
 
 // TC_F32_MMA=dmma: fp32 contractions through the DMMA micro-kernel (fp64 accumulation, one
 // rounding) instead of the default FFMA micro-kernel (fp32 accumulation).
 static bool f32_dmma() {
-  static const bool f = [] {
-    const char* e = getenv("TC_F32_MMA");
-    return e && !strcmp(e, "dmma");
-  }();
-  return f;
+  const char* e = getenv("TC_F32_MMA");
+  return e && !strcmp(e, "dmma");
 }
 
 // TC_GATHER=mixed|elem forces the gather mode of operands that are not all-vector (ablation);
 // by default the plan decides (Plan::a_elem / b_elem).
 static int gather_override() {
-  static const int g = [] {
-    const char* e = getenv("TC_GATHER");
-    if (e && !strcmp(e, "mixed")) return 1;
-    if (e && !strcmp(e, "elem")) return 2;
-    return 0;
-  }();
-  return g;
+  if (force_path() == 2) return 1;
+  const char* e = getenv("TC_GATHER");
+  if (e && !strcmp(e, "mixed")) return 1;
+  if (e && !strcmp(e, "elem")) return 2;
+  return 0;
 }
 
 // Size limits of the tiny-contraction kernel (log2 of C elements and of multiply-adds);
@@ -168,11 +179,8 @@ static void tiny_limits(int* mn, int* mnk) {
 }
 
 static bool f32_a_transpose() {
-  static const bool f = [] {
-    const char* e = getenv("TC_FFMA_AT");
-    return !(e && !strcmp(e, "0"));
-  }();
-  return f;
+  const char* e = getenv("TC_FFMA_AT");
+  return !(e && !strcmp(e, "0"));
 }
 
 static int get_tables(const Plan& p, DeviceTables** out) {
@@ -196,12 +204,13 @@ static int get_tables(const Plan& p, DeviceTables** out) {
   const int64_t V = p.dtype == TC_F64 ? 2 : 4;
   std::vector<uint8_t> fa = vec_flags(ta, padded((int64_t)ta.size()), V);
   std::vector<uint8_t> fb = vec_flags(tb, padded((int64_t)tb.size()), V);
-  if (force_scatter()) {
-    std::fill(fa.begin(), fa.end(), 0);
-    std::fill(fb.begin(), fb.end(), 0);
-  }
   e = upload_bytes(fa, &d->vA);
   if (e == cudaSuccess) e = upload_bytes(fb, &d->vB);
+  if (e == cudaSuccess)
+    e = upload_bytes(std::vector<uint8_t>(std::max(fa.size(), fb.size()), 0), &d->vZ);
+  // the uploads ran on the legacy stream (a pageable cudaMemcpy may return before its DMA has
+  // landed, cudaMemset is asynchronous): wait for them before any stream may read the tables
+  if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
   if (e != cudaSuccess) { delete d; return cuda_fail(e, "flag upload"); }
   p.dev.push_back(d);
   *out = d;
@@ -227,15 +236,17 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.C = C;
   a.rA = d->tab[0]; a.cA = d->tab[1]; a.rB = d->tab[2];
   a.cB = d->tab[3]; a.rC = d->tab[4]; a.cC = d->tab[5];
-  a.vA = d->vA; a.vB = d->vB;
+  const bool scatter_only = force_scatter();
+  a.vA = scatter_only ? d->vZ : d->vA;
+  a.vB = scatter_only ? d->vZ : d->vB;
   a.M = (int)p.m; a.N = (int)p.n; a.K = skip_ab ? 0 : (int)p.k;
   a.alpha = alpha; a.beta = beta;
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
-  a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0 && !force_scatter();
-  a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !force_scatter();
+  a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0 && !scatter_only;
+  a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !scatter_only;
   a.a_elem = gather_override() ? gather_override() == 2 : p.a_elem;
   a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
-  a.f32_a_transpose = f32_a_transpose() && !force_scatter();
+  a.f32_a_transpose = f32_a_transpose() && !scatter_only;
   a.c_lanes_n = p.c_unit_n;
   a.skinny_bu = p.skinny_bu;
   tiny_limits(&a.tiny_mn_log2, &a.tiny_mnk_log2);
@@ -245,6 +256,17 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   StreamFlags* sf = stream_flags(d->device, stream, a.flags_cap);
   a.flags = sf ? sf->flags : nullptr;
   a.wave_base = sf ? &sf->wave_base : nullptr;
+  if (sf) {
+    // epochs 1 .. 2^24 - 1 (sched.cuh); when they wrap, the flags are zeroed on the stream
+    // first, so a value from 2^24 launches ago cannot match
+    const unsigned n = sf->epoch.fetch_add(1, std::memory_order_relaxed);
+    const unsigned ep = n % 0xFFFFFFu + 1u;
+    if (ep == 1u && n != 0u) {
+      cudaError_t e = cudaMemsetAsync(sf->flags, 0, sizeof(int) * (size_t)a.flags_cap, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "flag reset");
+    }
+    a.flag_epoch = ep << 8;
+  }
   a.wave_sync = sf != nullptr && wave_sync();
   a.stream_k = a.flags != nullptr;
   a.f32_dmma = f32_dmma();
@@ -647,8 +669,21 @@ int tc_plan_create(tc_plan** plan, tc_dtype dtype, const tc_tensor* A, const tc_
 int tc_plan_execute(const tc_plan* plan, double alpha, const void* A, const void* B, double beta,
                     void* C, void* stream) {
   if (!plan) return fail(TC_ERR_ARG, "null plan");
-  return execute(*reinterpret_cast<const Plan*>(plan), alpha, A, B, beta, C,
-                 static_cast<cudaStream_t>(stream));
+  const Plan& p = *reinterpret_cast<const Plan*>(plan);
+  // the same alias check as tc_contract (reading R7), on the spans the plan recorded
+  const int64_t esz = p.dtype == TC_F64 ? 8 : 4;
+  auto bytes = [&](const void* d, int t, const char** lo, const char** hi) {
+    if (!d || p.span_lo[t] > p.span_hi[t]) return false;
+    *lo = static_cast<const char*>(d) + p.span_lo[t] * esz;
+    *hi = static_cast<const char*>(d) + (p.span_hi[t] + 1) * esz;
+    return true;
+  };
+  const char *c0, *c1, *x0, *x1;
+  if (bytes(C, 2, &c0, &c1))
+    for (int t = 0; t < 2; ++t)
+      if (bytes(t == 0 ? A : B, t, &x0, &x1) && x0 < c1 && c0 < x1)
+        return fail(TC_ERR_ALIAS, "C overlaps A or B");
+  return execute(p, alpha, A, B, beta, C, static_cast<cudaStream_t>(stream));
 }
 
 int tc_plan_destroy(tc_plan* plan) {

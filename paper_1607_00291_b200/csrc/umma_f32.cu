@@ -663,7 +663,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #endif
           // pair: each piece is published by both CTAs (two counts per piece)
           if (threadIdx.x == kEpi0 * 32)
-            while (ld_acquire(flag) != (kPair ? 2 * piece : piece)) __nanosleep(64);
+            wait_flag(flag, (int)(sched.epoch | (unsigned)(kPair ? 2 * piece : piece)));
           epi_sync();
 #ifdef TC_UMMA_TRACE
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
@@ -768,17 +768,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         else if constexpr (!kN256) mbar_arrive(&tempty[cb]);
       }
       if (split) {
-        // publish this piece; the last piece leaves the flag at 0, so the buffer is all zero
-        // again when the kernel ends (no per-launch reset)
+        // publish this piece (epoch-tagged: nothing is reset for the next launch)
         epi_sync();
         if (threadIdx.x == kEpi0 * 32) {
           __threadfence();
           if constexpr (kPair) {
-            // count this half; the second half of the last piece resets the flag
-            const int old = atomicAdd(flag, 1);
-            if (ke == sched.KT && old == 2 * piece + 1) st_release(flag, 0);
-          } else {
-            st_release(flag, ke < sched.KT ? piece + 1 : 0);
+            count_flag(flag, sched.epoch);   // one count per CTA of the pair
+          } else if (ke < sched.KT) {
+            st_release(flag, (int)(sched.epoch | (unsigned)(piece + 1)));
           }
         }
       }
@@ -928,6 +925,7 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
   Sched sc = make_sched(T, KT, units, sk, pp ? atoi(pp) : 70, min_sk);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) sc = make_sched(T, KT, units, false);
   sc.wave_sync = 0;
+  sc.epoch = a.flag_epoch;
   const int nunits = sc.D > 0 ? (sc.D < sc.P ? sc.D : sc.P) : sc.P_sk;
   const float* pA = static_cast<const float*>(a.A);
   const float* pB = static_cast<const float*>(a.B);
