@@ -72,6 +72,8 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-ttdt", action="store_true")
+    ap.add_argument("--smtc", action="store_true",
+                    help="also time the all-scatter ablation (TC_FORCE_PATH=scatter, per call)")
     ap.add_argument("--family", default="baseline", choices=["baseline", "f1", "f2"])
     args = ap.parse_args()
     for case in cases(args.only, args.family):
@@ -98,11 +100,31 @@ def main():
                "hbm_gbs": round(A.element_size() * (A.numel() + B.numel() + C.numel() *
                                                      (2 if case.beta != 0 else 1)) / t / 1e6, 1),
                "force_path": os.environ.get("TC_FORCE_PATH", "")}
-        if not args.no_ttdt and fl < 2e12:
+        if args.smtc:
+            os.environ["TC_FORCE_PATH"] = "scatter"
             try:
-                tt = timeit(ttdt(case, A, B, C.clone()), reps)
+                ts = timeit(lambda: tc.contract(case.spec, A, B, C, case.alpha, case.beta), reps)
+            finally:
+                del os.environ["TC_FORCE_PATH"]
+            row.update(smtc_ms=round(ts, 4), smtc_gflops=round(fl / ts / 1e6, 1),
+                       bsmtc_speedup_vs_smtc=round(ts / t, 3))
+        if not args.no_ttdt:
+            try:
+                C2 = C.clone()
+                run = ttdt(case, A, B, C2)
+                torch.cuda.synchronize()
+                base = torch.cuda.memory_allocated()
+                torch.cuda.reset_peak_memory_stats()
+                run()
+                torch.cuda.synchronize()
+                ws = torch.cuda.max_memory_allocated() - base
+                tt = timeit(run, reps)
+                # TTDT's extra device memory: the matricised copies of A and B and the GEMM
+                # output before its transpose-and-sum (fig:TTDT); this path: 0
                 row.update(ttdt_ms=round(tt, 4), ttdt_gflops=round(fl / tt / 1e6, 1),
-                           speedup_vs_ttdt=round(tt / t, 3))
+                           speedup_vs_ttdt=round(tt / t, 3), ttdt_workspace_bytes=int(ws),
+                           operand_bytes=int(A.element_size() * (A.numel() + B.numel() + C.numel())))
+                del C2
             except torch.OutOfMemoryError:
                 pass
         print(json.dumps(row), flush=True)
