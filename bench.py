@@ -5,7 +5,8 @@ Workload (BASELINE.json configs[4], the 1/2/4/8-GPU config; fits one GPU): cfg5
   M x N x K = 55296 x 27648 x 27648 (8.45e13 flops per step), 30.6 GB of operands (>> 126 MB L2).
 A step is one full contraction pass (all §8(a) rows: plan lookup, staging, DMMA, epilogue).
 With N GPUs, C is sharded over free blocks of (a, b, c) after one NCCL
-broadcast of A and B from rank 0; K is never split, so there is no data-path
+distribution of A and B from rank 0 (each rank receives the slabs its block reads,
+paper_1607_00291_b200/dist.py); K is never split, so there is no data-path
 collective. Total work is fixed as N grows -> "scaling": "strong".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--small]
@@ -248,6 +249,19 @@ def timed_loop(fn, steps, stream, world):
     return total, per
 
 
+def distribution_bytes(case, world, scheme):
+    """Modelled bytes of the operand distribution: what rank 0 sends and what each other rank
+    receives (dist.plan_traffic; a ring broadcast sends each byte out of its root once)."""
+    from paper_1607_00291_b200 import dist as tdist
+    ops = [(case.lab_a, 8), (case.lab_b, 8)]
+    if scheme == "broadcast":
+        full = sum(8 * math.prod(case.shape(lab)) for lab, _ in ops)
+        return {"scheme": "broadcast", "src_egress": full, "recv_per_rank": full}
+    m = tdist.plan_traffic(world, case.lens, SHARD_LABELS, ops)
+    return {"scheme": "slabs (send to slab-group leader + group broadcast)",
+            "src_egress": m["src_egress"], "recv_per_rank": max(m["recv"])}
+
+
 def run_native(args):
     world, rank, local = dist_env()
     if args.gpus != world and world > 1:
@@ -264,8 +278,9 @@ def run_native(args):
     stream = torch.cuda.current_stream()
 
     # -- inputs: seeded on rank 0's GPU and distributed once over NCCL (the one exchange step):
-    # by default each rank receives only the A and B slabs its block of C reads (point-to-point,
-    # dist.distribute_slabs); --distribute broadcast sends everyone the full operands instead
+    # by default each rank receives only the A and B slabs its block of C reads (dist.distribute:
+    # rank 0 sends each distinct slab once to its group's leader, which broadcasts it within the
+    # group); --distribute broadcast sends everyone the full operands instead
     t_b0 = time.perf_counter()
     slabs = world > 1 and args.distribute == "slabs"
     A = B = None
@@ -287,8 +302,8 @@ def run_native(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if slabs:
-            As, Bs, recv_elems = tdist.distribute_slabs(spec, A, B, lens, SHARD_LABELS, world,
-                                                        rank, dtype=torch.float64, device="cuda")
+            As, Bs, recv_elems, _ = tdist.distribute_slabs(spec, A, B, lens, SHARD_LABELS, world,
+                                                           rank, dtype=torch.float64, device="cuda")
             A = B = None   # rank 0 keeps dense copies of its own slabs, like every other rank
         else:
             flatA = torch.as_strided(A, (A.numel(),), (1,))
@@ -297,6 +312,9 @@ def run_native(args):
         e1.record()
         torch.cuda.synchronize()
         bcast_ms = e0.elapsed_time(e1)
+        t = torch.tensor([bcast_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)     # the distribution ends on its slowest rank
+        bcast_ms = float(t.item())
         torch.cuda.empty_cache()
     cshape = tdist.shard_shape(case.lab_c, lens, ranges)
     C = W.colmajor_view(torch.full((math.prod(cshape),), float("nan"), dtype=torch.float64,
@@ -379,7 +397,12 @@ def run_native(args):
             t = torch.tensor([el], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
+        # at N > 1 each rank's inputs are its own slabs in host memory (one node: every GPU
+        # copies over its own PCIe link); the device-side distribution of the resident-input
+        # run is reported beside it as if it were paid once per step (value_incl_distribution)
         e2e = {"value": round(flops_total / (el / esteps) / 1e9, 2), "unit": "GFLOP/s",
+               "value_incl_distribution": None if bcast_ms is None else round(
+                   flops_total / (el / esteps + bcast_ms * 1e-3) / 1e9, 2),
                "h2d_bytes_per_step": (hA.numel() + hB.numel()) * 8 * world,
                "d2h_bytes_per_step": hC.numel() * 8 * world,
                "steps": esteps, "ms_per_step": round(1e3 * el / esteps, 2),
@@ -415,7 +438,10 @@ def run_native(args):
                                        else "NCCL broadcast of A,B")),
                    "shard_ranges_rank0": ranges, "l2": "inputs larger than L2 (30.6 GB >> 126 MB)",
                    "distribute": args.distribute if world > 1 else None,
-                   "distribute_ms": bcast_ms, "received_elems_rank": recv_elems, "plan": info},
+                   "distribute_ms": bcast_ms, "received_elems_rank": recv_elems,
+                   "distribution_bytes": None if world == 1 else distribution_bytes(
+                       case, world, args.distribute),
+                   "plan": info},
         "pct_fp64_peak": round(100 * value / 1e3 / (peak * world), 2),
         "same_size_gemm": None if gemm_tf is None else {
             "kind": "cuBLAS DGEMM (torch.mm float64) of the rank-0 shard's M x N x K",

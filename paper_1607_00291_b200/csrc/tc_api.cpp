@@ -11,12 +11,22 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "kernels.hpp"
 #include "plan.hpp"
 #include "tc.h"
 
 namespace tcb {
+
+// NVTX ranges around the entry points and the host path's stages (visible in nsys / ncu
+// --nvtx; a push/pop costs nanoseconds when no tool is attached).
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 static thread_local std::string g_detail;
 
@@ -302,6 +312,7 @@ static int check_tensor(const tc_tensor* t, const char* name) {
 
 static int get_plan(tc_dtype dtype, const tc_tensor* A, const tc_tensor* B, const tc_tensor* C,
                     std::shared_ptr<Plan>* out) {
+  Nvtx range("tc_plan_lookup");
   int rc;
   if ((rc = check_tensor(A, "A")) || (rc = check_tensor(B, "B")) || (rc = check_tensor(C, "C")))
     return rc;
@@ -398,6 +409,7 @@ constexpr int64_t kHostChunkMinBytes = 64ll << 20;
 
 static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                          double beta, const tc_tensor* C, cudaStream_t s) {
+  Nvtx range("tc_contract_host");
   std::shared_ptr<Plan> full;
   int rc = get_plan(dtype, A, B, C, &full);
   if (rc != TC_OK) return rc;
@@ -531,6 +543,7 @@ static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const
   };
 
   for (int i = 0; i < nch && e == cudaSuccess && rc == TC_OK; ++i) {
+    Nvtx chunk_range("tc_contract_host chunk (H2D, kernels, D2H enqueue)");
     const int64_t x0 = i * best_q, l = best_c < 0 ? 0 : std::min(best_q, best_len - x0);
     // the chunk's address spans: x restricted to [x0, x0 + l)
     Piece pp[3];
@@ -608,6 +621,7 @@ static tc_tensor restrict_label(const tc_tensor* T, char lbl, int64_t lo, int64_
 
 int tc_contract(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                 double beta, const tc_tensor* C, void* stream) {
+  Nvtx range("tc_contract");
   std::shared_ptr<Plan> p;
   int rc = get_plan(dtype, A, B, C, &p);
   if (rc != TC_OK) return rc;
@@ -669,6 +683,7 @@ int tc_plan_create(tc_plan** plan, tc_dtype dtype, const tc_tensor* A, const tc_
 int tc_plan_execute(const tc_plan* plan, double alpha, const void* A, const void* B, double beta,
                     void* C, void* stream) {
   if (!plan) return fail(TC_ERR_ARG, "null plan");
+  Nvtx range("tc_plan_execute");
   const Plan& p = *reinterpret_cast<const Plan*>(plan);
   // the same alias check as tc_contract (reading R7), on the spans the plan recorded
   const int64_t esz = p.dtype == TC_F64 ? 8 : 4;
