@@ -100,6 +100,18 @@ __device__ __forceinline__ void wait_flag(const int* flag, int target) {
     if (global_ns() - t0 > kFlagTimeoutNs) flag_timeout(flag, target);
   }
 }
+// Pair form (two arrivals per piece, count_flag): wait until this launch's count reaches
+// `target`. The two CTAs of a pair wait for the same count, and the first one through may add
+// its own arrival before the other has looked, so the wait is for `>=`, not `==`.
+__device__ __forceinline__ void wait_flag_ge(const int* flag, unsigned epoch, int target) {
+  auto done = [&](unsigned v) { return (v & ~0xffu) == epoch && (int)(v & 0xffu) >= target; };
+  if (done((unsigned)ld_acquire(flag))) return;
+  const unsigned long long t0 = global_ns();
+  while (!done((unsigned)ld_acquire(flag))) {
+    __nanosleep(64);
+    if (global_ns() - t0 > kFlagTimeoutNs) flag_timeout(flag, (int)(epoch | (unsigned)target));
+  }
+}
 // Count one arrival on a flag of this launch's epoch: a value from another epoch counts as 0.
 __device__ __forceinline__ void count_flag(int* flag, unsigned epoch) {
   int old = ld_acquire(flag);

@@ -663,7 +663,10 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #endif
           // pair: each piece is published by both CTAs (two counts per piece)
           if (threadIdx.x == kEpi0 * 32)
-            wait_flag(flag, (int)(sched.epoch | (unsigned)(kPair ? 2 * piece : piece)));
+          {
+            if constexpr (kPair) wait_flag_ge(flag, sched.epoch, 2 * piece);
+            else wait_flag(flag, (int)(sched.epoch | (unsigned)piece));
+          }
           epi_sync();
 #ifdef TC_UMMA_TRACE
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr2));
@@ -812,15 +815,15 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         if (chunk_start) {
           const int cb = ch % kChunkBufs;
           if (ch >= kChunkBufs) {
-            if constexpr (kPair) PWAIT(4, mbar_wait_cluster(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
-            else PWAIT(4, mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1));
+            if constexpr (kPair) { PWAIT(4, mbar_wait_cluster(&tempty[cb], ((ch / kChunkBufs) - 1) & 1)); }
+            else { PWAIT(4, mbar_wait(&tempty[cb], ((ch / kChunkBufs) - 1) & 1)); }
           }
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
           d = tmem + (uint32_t)(cb * kChunkCols);
         }
         const int s = it % STAGES;
-        if constexpr (kPair) PWAIT(5, mbar_wait_cluster(&conv[s], (it / STAGES) & 1));
-        else PWAIT(5, mbar_wait(&conv[s], (it / STAGES) & 1));
+        if constexpr (kPair) { PWAIT(5, mbar_wait_cluster(&conv[s], (it / STAGES) & 1)); }
+        else { PWAIT(5, mbar_wait(&conv[s], (it / STAGES) & 1)); }
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
           const float* st = stage0 + s * kStage;

@@ -70,13 +70,17 @@ def cases(only, family):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
+    ap.add_argument("--match", default="", help="regular expression on the case name")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--no-ttdt", action="store_true")
     ap.add_argument("--smtc", action="store_true",
                     help="also time the all-scatter ablation (TC_FORCE_PATH=scatter, per call)")
     ap.add_argument("--family", default="baseline", choices=["baseline", "f1", "f2"])
     args = ap.parse_args()
+    import re
     for case in cases(args.only, args.family):
+        if args.match and not re.search(args.match, case.name):
+            continue
         A, B, C = W.make_tensors(case, "cuda")
         if case.c_init == "nan":
             C.zero_()
