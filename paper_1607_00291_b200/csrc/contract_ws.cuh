@@ -65,6 +65,11 @@ constexpr int kEpiWarpFloats = 32 * kEpiLD;
 #define TC_DMMA_STAGED 0
 #endif
 constexpr int kEpiDLD = 16 + 4;
+// Edge tiles multiply only the m16 / n8 blocks of each warp tile that hold data (stage_edge);
+// TC_DMMA_EDGE=0 builds the variant without (measurement A/B).
+#ifndef TC_DMMA_EDGE
+#define TC_DMMA_EDGE 1
+#endif
 constexpr int kEpiWarpDoubles = 32 * kEpiDLD;
 constexpr int kSmemLimit = 232448;   // 227 KB of dynamic shared memory per CTA
 // Tile rasterisation group height. With K in the tens of thousands a CTA's A and B panels are
@@ -409,6 +414,35 @@ struct MicroDmma {
                      acc[2 * i + 1][2 * j + 1], a[i][0], a[i][1], b[j]);
     }
   }
+  // ragged tile edges (and / or the last, partial K step): only the ni m16 blocks and nj n8
+  // blocks of the warp tile that hold rows < M and columns < N, and the nk4 groups of 4 k that
+  // hold data (warp-uniform bounds). A 128 x 128 tile over a 323-row edge (fig:bench's
+  // ab-cad-dcb) then multiplies 336 rows instead of 384.
+  __device__ __forceinline__ void stage_edge(const T* as, const T* bs, int nk4, int ni, int nj) {
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      if (kk >= nk4) break;
+      double a[4][2], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i][0] = static_cast<double>(as[AL::at(wm + 16 * i + g, 4 * kk + t)]);
+        a[i][1] = static_cast<double>(as[AL::at(wm + 16 * i + g + 8, 4 * kk + t)]);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        b[j] = static_cast<double>(bs[BL::at(4 * kk + t, wn + 8 * j + g)]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i >= ni) break;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= nj) break;
+          dmma16x8x4(acc[2 * i][2 * j], acc[2 * i][2 * j + 1], acc[2 * i + 1][2 * j],
+                     acc[2 * i + 1][2 * j + 1], a[i][0], a[i][1], b[j]);
+        }
+      }
+    }
+  }
   // last, partial K step: only the nk4 groups of 4 k that hold data (the rest is zero-filled)
   __device__ __forceinline__ void stage_tail(const T* as, const T* bs, int nk4) {
     for (int kk = 0; kk < nk4; ++kk) {
@@ -747,6 +781,19 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       }
     }
     mk.zero();
+    // m16 / n8 blocks of this warp's 64 x 32 tile that hold rows < M, columns < N
+    int edge_mi = 4, edge_nj = 4;
+    if constexpr (!FFMA && TC_DMMA_EDGE) {
+      edge_mi = (M - (m0 + mk.wm) + 15) / 16;
+      edge_nj = (N - (n0 + mk.wn) + 7) / 8;
+      edge_mi = edge_mi < 0 ? 0 : (edge_mi > 4 ? 4 : edge_mi);
+      edge_nj = edge_nj < 0 ? 0 : (edge_nj > 4 ? 4 : edge_nj);
+    }
+    // the skipping path runs only where it saves at least half of the warp's MMAs: its loads
+    // are less well pipelined, and an edge warp that is slower per K step than its neighbours
+    // holds the whole CTA's ring (measured: ragged cfg4 shapes 3-12% slower when every edge warp
+    // took it; profiles/r02/ab_dmma_edge.txt)
+    const bool interior = edge_mi * edge_nj > 8;
     for (int kt = kb; kt < ke; ++kt, ++it) {
       const int s = it % STAGES;
       mbar_wait(&full[s], (it / STAGES) & 1);
@@ -756,8 +803,13 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
         mk.stage(As + s * AL::STAGE, Bs + s * BL::STAGE);
       } else {
         const int krem = K - kt * BK;
-        if (krem >= BK) mk.stage(As + s * AL::STAGE, Bs + s * BL::STAGE);
-        else mk.stage_tail(As + s * AL::STAGE, Bs + s * BL::STAGE, (krem + 3) / 4);
+        if (interior) {
+          if (krem >= BK) mk.stage(As + s * AL::STAGE, Bs + s * BL::STAGE);
+          else mk.stage_tail(As + s * AL::STAGE, Bs + s * BL::STAGE, (krem + 3) / 4);
+        } else {
+          mk.stage_edge(As + s * AL::STAGE, Bs + s * BL::STAGE, krem >= BK ? BK / 4 : (krem + 3) / 4,
+                        edge_mi, edge_nj);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);

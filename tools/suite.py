@@ -56,6 +56,8 @@ def ttdt(case, A, B, C):
 
 
 def cases(only, family):
+    if family == "all":
+        return [c for f in ("baseline", "f1", "f2") for c in cases(only, f)]
     if family == "f2":
         out = [W.fig_bench(i) for i in range(24)]
     elif family == "f1":
@@ -75,7 +77,7 @@ def main():
     ap.add_argument("--no-ttdt", action="store_true")
     ap.add_argument("--smtc", action="store_true",
                     help="also time the all-scatter ablation (TC_FORCE_PATH=scatter, per call)")
-    ap.add_argument("--family", default="baseline", choices=["baseline", "f1", "f2"])
+    ap.add_argument("--family", default="baseline", choices=["baseline", "f1", "f2", "all"])
     args = ap.parse_args()
     import re
     for case in cases(args.only, args.family):
