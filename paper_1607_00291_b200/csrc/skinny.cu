@@ -15,6 +15,7 @@
 // Roles: X = A (rows = I, tables rA / cA), Y = B (cB / rB) when the small free bundle is J;
 // X = B, Y = A (the transposed problem C^T = B^T A^T) when it is I.
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_runtime.h>
 
@@ -232,10 +233,16 @@ static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
   static std::atomic<int> attr[kMaxDevices];
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int nblk = (a.R + kRows - 1) / kRows;
-  // low arithmetic intensity (small resident operand, e.g. N = K = 32: HBM-bound) runs three
-  // CTAs per SM's worth of grid, more blocks in flight; larger ones one (f2 strings: N = K = 32
-  // 0.88 -> 0.98 of DGEMM, N = K = 76 -3..-5% with three; profiles/r01/ab_skinny_grid.txt)
-  const int cps = a.KP * a.NP <= 48 * 48 ? 3 : 1;
+  // low arithmetic intensity (small resident operand, e.g. N = K = 32: HBM-bound) runs four
+  // CTAs per SM's worth of grid with a 2-deep ring, more CTAs in flight; larger ones one CTA with
+  // a 3-deep ring (f2 strings: N = K = 32 0.88 -> 0.98 of DGEMM with three CTAs,
+  // profiles/r01/ab_skinny_grid.txt; four CTAs x 2 buffers 3.34 -> 3.58 TB/s,
+  // profiles/r02/ab_skinny_grid.txt; N = K = 76 -3..-5% with three)
+  static const int cps_env = [] {   // measurement override (TC_SKINNY_CPS)
+    const char* e = getenv("TC_SKINNY_CPS");
+    return e ? atoi(e) : 0;
+  }();
+  const int cps = cps_env > 0 ? cps_env : (a.KP * a.NP <= 48 * 48 ? 4 : 1);
   const int grid = nblk < cps * nsm ? nblk : cps * nsm;
   kern<<<grid, kThreads, smem, s>>>(a);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
@@ -245,6 +252,13 @@ static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
 // the HBM-bound f2 strings (0.84 -> 0.64 of DGEMM).
 template <typename IDX, bool ROWS_UNIT, int NW>
 static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
+  static const int nbuf_env = [] {   // measurement override (TC_SKINNY_NBUF = 2 | 3 | 4)
+    const char* e = getenv("TC_SKINNY_NBUF");
+    return e ? atoi(e) : 0;
+  }();
+  const int nbuf = nbuf_env > 0 ? nbuf_env : (a.KP * a.NP <= 48 * 48 ? 2 : kBufs);
+  if (nbuf == 2) return launch_nb<IDX, ROWS_UNIT, NW, 2>(a, nsm, s);
+  if (nbuf == 4) return launch_nb<IDX, ROWS_UNIT, NW, 4>(a, nsm, s);
   return launch_nb<IDX, ROWS_UNIT, NW, kBufs>(a, nsm, s);
 }
 
