@@ -30,6 +30,8 @@ struct LaunchArgs {
   bool a_vec_m, b_vec_k, idx64, f32;
   // every pair of the operand's gather direction is contiguous and 16-byte aligned
   bool a_vec_all, b_vec_all;
+  // fp32: every 8-byte pair of the operand's gather direction contiguous and 8-byte aligned
+  bool a_vec2_all, b_vec2_all;
   // gather mode per operand (contract_ws.cuh GatherSel): 0 vectors, 1 per-vector check,
   // 2 coalesced elements; set by launch_contract from a_vec_all / b_vec_all and the plan
   int a_mode, b_mode;

@@ -418,6 +418,12 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
                                 : vec_blocks_all(p->kscat[1], p->kscat[0], V);
     p->b_pairs_all = p->b_vec_k ? vec_blocks_all(p->kscat[2], p->kscat[3], V)
                                 : vec_blocks_all(p->kscat[3], p->kscat[2], V);
+    if (dtype == TC_F32) {
+      p->a_pairs2_all = p->a_vec_m ? vec_blocks_all(p->kscat[0], p->kscat[1], 2)
+                                   : vec_blocks_all(p->kscat[1], p->kscat[0], 2);
+      p->b_pairs2_all = p->b_vec_k ? vec_blocks_all(p->kscat[2], p->kscat[3], 2)
+                                   : vec_blocks_all(p->kscat[3], p->kscat[2], 2);
+    }
   }
   // Gather mode of an operand that is not all-vector (contract_ws.cuh GatherSel), measured on
   // the cfg4 / f2 suites (profiles/r01/suite_gather_ab.txt): for fp32 the coalesced element

@@ -73,6 +73,8 @@ struct Plan {
   bool idx64 = false;
   // whole-operand block-scatter check at 16-byte granularity (see vec_blocks_all in plan.cpp)
   bool a_pairs_all = false, b_pairs_all = false;
+  // the same at 8-byte granularity (fp32: pairs of floats), for the tcgen05 kernel's 8-byte gathers
+  bool a_pairs2_all = false, b_pairs2_all = false;
   // gather mode for operands that are not all-vector: coalesced element copies (true) or the
   // per-vector check (false), from the share of vectors that qualify (plan.cpp)
   bool a_elem = true, b_elem = true;

@@ -254,6 +254,8 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.a_vec_m = p.a_vec_m; a.b_vec_k = p.b_vec_k; a.idx64 = p.idx64; a.f32 = p.dtype == TC_F32;
   a.a_vec_all = p.a_pairs_all && (reinterpret_cast<uintptr_t>(a.A) % 16) == 0 && !scatter_only;
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !scatter_only;
+  a.a_vec2_all = p.a_pairs2_all && (reinterpret_cast<uintptr_t>(a.A) % 8) == 0 && !scatter_only;
+  a.b_vec2_all = p.b_pairs2_all && (reinterpret_cast<uintptr_t>(a.B) % 8) == 0 && !scatter_only;
   a.a_elem = gather_override() ? gather_override() == 2 : p.a_elem;
   a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
   a.f32_a_transpose = f32_a_transpose() && !scatter_only;

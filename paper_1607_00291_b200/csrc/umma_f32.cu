@@ -340,12 +340,91 @@ struct GatherVM {
   }
 };
 
-// operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors
+// 8-byte pair gathers (the block-scatter decision at 2-float granularity, a_vec2_all /
+// b_vec2_all): where the 16-byte vectors of an operand are not all contiguous and aligned but its
+// pairs are (odd lengths break vectors of four more often than pairs: 26 of cfg4's 40 operands
+// qualify against 17), half the copy instructions of the element gathers -- the producers of the
+// element-gather cases issue one 4-byte cp.async per element and are bound by that (~8 cycles
+// each, profiles/r02/umma_prof_roles.txt).
+//  GatherP2K: pairs along K (4 consecutive... lanes = 4 rows x 8 pairs = 16 consecutive k) into
+//             the K-major staging layout (a pair never straddles a core-matrix row)
+//  GatherP2M: pairs along the rows (A only) into the [k][m] staging of GatherVM; lanes = 32 pairs
+//             = 64 consecutive m at one k
+template <typename IDX, int CH = kChunk, int ROWS = 128>
+struct GatherP2K {
+  static constexpr int NR = ROWS / 4 / kPW;          // row groups of 4 per warp
+  IDX ro[NR];
+  uint32_t rv;
+  IDX ko[2];
+  __device__ __forceinline__ static int row(int w, int i, int l) { return 4 * (w * NR + i) + (l >> 3); }
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+    rv = 0;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int r = base + row(w, i, l);
+      ro[i] = rtab[r];
+      rv |= (r < extent ? 1u : 0u) << i;
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) ko[h] = __ldg(ktab + k0 + 16 * h + 2 * (l & 7));
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int kk = 16 * h + 2 * (l & 7);
+      const bool kin = k0 + kk < K;                  // K is even here
+#pragma unroll
+      for (int i = 0; i < NR; ++i)
+        cp_async8(sm + tile_off<CH>(row(w, i, l), kk), g + (ro[i] + ko[h]), kin && ((rv >> i) & 1u));
+    }
+  }
+};
+
+template <typename IDX>
+struct GatherP2M {
+  static constexpr int NKW = BK / kPW;               // k rows per warp
+  IDX ro[2];
+  bool rv[2];
+  IDX ko[NKW];
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = base + 64 * h + 2 * l;
+      ro[h] = rtab[r];
+      rv[h] = r < extent;                            // M is even here
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    const int w = (threadIdx.x >> 5);
+#pragma unroll
+    for (int j = 0; j < NKW; ++j) ko[j] = __ldg(ktab + k0 + w * NKW + j);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int j = 0; j < NKW; ++j) {
+      const int k = w * NKW + j;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        cp_async8(sm + k * BM + 64 * h + 2 * l, g + (ro[h] + ko[j]), rv[h] && k0 + k < K);
+    }
+  }
+};
+
+// operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors,
+// 5 K pairs, 6 row pairs (A)
 template <typename IDX, int MODE, int CH = kChunk, int ROWS = 128> struct GatherSel;
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 0, CH, R> { using type = Gather<IDX, false, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 1, CH, R> { using type = Gather<IDX, true, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 2, CH, R> { using type = GatherVK<IDX, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 3, CH, R> { using type = GatherVM<IDX>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 5, CH, R> { using type = GatherP2K<IDX, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 6, CH, R> { using type = GatherP2M<IDX>; };
 
 #ifdef TC_UMMA_PROF
 // measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
@@ -583,7 +662,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           for (int c = 0; c < KC / 4; ++c) {
             const int k = kc0 + 4 * c;
             float4 x;
-            if constexpr (A_MODE == 3) {   // [k][m] staging
+            if constexpr (A_MODE == 3 || A_MODE == 6) {   // [k][m] staging
               x = make_float4(st[k * BM + row], st[(k + 1) * BM + row], st[(k + 2) * BM + row],
                               st[(k + 3) * BM + row]);
             } else {
@@ -971,36 +1050,64 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
 // 0 = not applicable, 1 = launched, -1 = CUDA error.
 int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   if (!a.f32 || a.idx64 || a.K < 1) return 0;
-#ifdef TC_UMMA_ELEM_ONLY
-  const int am = a.a_vec_m ? 0 : 1;
-  const int bm = a.b_vec_k ? 1 : 0;
-#else
-  const int am = a.a_vec_m ? (a.a_vec_all ? 3 : 0) : (a.a_vec_all ? 2 : 1);
-  const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : 1) : 0;
-#endif
   using namespace TC_UMMA_NS;
+  // 8-byte pair gathers where the operand's pairs (not all its vectors) are contiguous and
+  // aligned; TC_UMMA_PAIRS=0 turns them off (measurement A/B)
+  const char* pe2 = getenv("TC_UMMA_PAIRS");
+  const bool pairs = !kPair && !(pe2 && !strcmp(pe2, "0"));
+  const bool a2 = pairs && a.a_vec2_all, b2 = pairs && a.b_vec2_all;
 #ifdef TC_UMMA_ELEM_ONLY
-  switch (am * 3 + bm) {
+  const int am = a.a_vec_m ? (a2 ? 6 : 0) : (a2 ? 5 : 1);
+  const int bm = a.b_vec_k ? (b2 ? 5 : 1) : 0;
+  switch (am * 10 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
     case 1: return launch_dir<int, 0, 1>(a, stream);
-    case 3: return launch_dir<int, 1, 0>(a, stream);
-    default: return launch_dir<int, 1, 1>(a, stream);
+    case 5: return launch_dir<int, 0, 5>(a, stream);
+    case 10: return launch_dir<int, 1, 0>(a, stream);
+    case 11: return launch_dir<int, 1, 1>(a, stream);
+    case 15: return launch_dir<int, 1, 5>(a, stream);
+    case 50: return launch_dir<int, 5, 0>(a, stream);
+    case 51: return launch_dir<int, 5, 1>(a, stream);
+    case 55: return launch_dir<int, 5, 5>(a, stream);
+    case 60: return launch_dir<int, 6, 0>(a, stream);
+    case 61: return launch_dir<int, 6, 1>(a, stream);
+    default: return launch_dir<int, 6, 5>(a, stream);
   }
-#endif
-  switch (am * 3 + bm) {
+#else
+  const int am = a.a_vec_m ? (a.a_vec_all ? 3 : (a2 ? 6 : 0)) : (a.a_vec_all ? 2 : (a2 ? 5 : 1));
+  const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : (b2 ? 5 : 1)) : 0;
+  if constexpr (!kPair) {
+    switch (am * 10 + bm) {
+      case 5: return launch_dir<int, 0, 5>(a, stream);
+      case 15: return launch_dir<int, 1, 5>(a, stream);
+      case 25: return launch_dir<int, 2, 5>(a, stream);
+      case 35: return launch_dir<int, 3, 5>(a, stream);
+      case 50: return launch_dir<int, 5, 0>(a, stream);
+      case 51: return launch_dir<int, 5, 1>(a, stream);
+      case 52: return launch_dir<int, 5, 2>(a, stream);
+      case 55: return launch_dir<int, 5, 5>(a, stream);
+      case 60: return launch_dir<int, 6, 0>(a, stream);
+      case 61: return launch_dir<int, 6, 1>(a, stream);
+      case 62: return launch_dir<int, 6, 2>(a, stream);
+      case 65: return launch_dir<int, 6, 5>(a, stream);
+      default: break;
+    }
+  }
+  switch (am * 10 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
     case 1: return launch_dir<int, 0, 1>(a, stream);
     case 2: return launch_dir<int, 0, 2>(a, stream);
-    case 3: return launch_dir<int, 1, 0>(a, stream);
-    case 4: return launch_dir<int, 1, 1>(a, stream);
-    case 5: return launch_dir<int, 1, 2>(a, stream);
-    case 6: return launch_dir<int, 2, 0>(a, stream);
-    case 7: return launch_dir<int, 2, 1>(a, stream);
-    case 8: return launch_dir<int, 2, 2>(a, stream);
-    case 9: return launch_dir<int, 3, 0>(a, stream);
-    case 10: return launch_dir<int, 3, 1>(a, stream);
+    case 10: return launch_dir<int, 1, 0>(a, stream);
+    case 11: return launch_dir<int, 1, 1>(a, stream);
+    case 12: return launch_dir<int, 1, 2>(a, stream);
+    case 20: return launch_dir<int, 2, 0>(a, stream);
+    case 21: return launch_dir<int, 2, 1>(a, stream);
+    case 22: return launch_dir<int, 2, 2>(a, stream);
+    case 30: return launch_dir<int, 3, 0>(a, stream);
+    case 31: return launch_dir<int, 3, 1>(a, stream);
     default: return launch_dir<int, 3, 2>(a, stream);
   }
+#endif
 }
 
 }  // namespace tcb

@@ -457,6 +457,37 @@ def test_f32_vector_gathers(spec, mnk):
 
 
 @pytest.mark.usefixtures("both_f32_paths")
+@pytest.mark.parametrize("spec", ["mn-mk-kn", "mn-km-nk", "mn-mk-nk", "mn-km-kn"])
+@pytest.mark.parametrize("mnk", [(262, 198, 102), (130, 390, 34), (514, 134, 262)])
+def test_f32_pair_gathers(spec, mnk):
+    """Even lengths that are not multiples of 4: every 8-byte pair of an operand's gather
+    direction is contiguous and aligned but its 16-byte vectors are not, so the tcgen05 kernel's
+    8-byte pair gathers run (K pairs into the K-major layout, M pairs of A into the [k][m]
+    staging); ragged tiles in M, N and K; also at a 4-byte offset (pairs misaligned: element
+    gathers)."""
+    lc, la, lb = spec.split("-")
+    case = W.Case("f32pair_" + spec, lc, la, lb, dict(zip("mnk", mnk)), dtype=torch.float32,
+                  alpha=0.75, beta=-0.5, c_init="dist", seed=43)
+    info = tc().Plan(case.spec, torch.float32, [case.shape(x) for x in (la, lb, lc)],
+                     [W.colmajor_strides(case.shape(x)) for x in (la, lb, lc)]).info()
+    assert info["m"] % 2 == 0 and info["k"] % 2 == 0
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+    # the same operands one element off a 16-byte boundary
+    A, B, C = W.make_tensors(case, "cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    bufA = torch.empty(A.numel() + 1, device="cuda")
+    Ad = W.colmajor_view(bufA[1:], list(A.shape))
+    Ad.copy_(A.cuda())
+    Cd = C.cuda()
+    tc().contract(case.spec, Ad, B.cuda(), Cd, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    assert torch.equal(Cd.cpu(), ref)
+
+
+@pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.usefixtures("both_small_paths")
 def test_f32_misaligned_views():
     g = torch.Generator().manual_seed(4)
