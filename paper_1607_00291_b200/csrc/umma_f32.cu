@@ -132,6 +132,10 @@ __device__ __forceinline__ uint32_t tmem_u32_addr(const void* p) { return smem_u
 // gather writes in one instruction on different banks. (The MN-major tf32 operand mode left the
 // accumulator at zero on this part, tools/calib/umma_tf32_test.cu, so both operands are K-major.)
 constexpr int kChunk = 128 * 4 + 16;
+// K chunk stride of an operand's staging (floats): the one-row-per-instruction K gather (mode 7)
+// writes eight consecutive chunks per instruction, which a 64-byte pad would put on two bank
+// groups; a 16-byte pad spreads them over all banks
+template <int BASE, int MODE> constexpr int chunk_stride() { return BASE + (MODE == 7 ? 4 : 16); }
 template <int CH = kChunk>
 __device__ __forceinline__ int tile_off(int r, int k) {
   return (k >> 2) * CH + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
@@ -416,8 +420,73 @@ struct GatherP2M {
   }
 };
 
+// Element gathers with one line per warp instruction where the operand allows it. The 8 x 4 and
+// 4 x 8 lane mappings above fill whole 32-byte sectors of a contiguous operand but touch four
+// 128-byte lines per instruction, and where the traversal interleaves dimensions (R17
+// sub-division) up to 16; an L1 line costs ~2 cycles per instruction (B300_MICROARCH), and these
+// gathers are what bounds the producer warps (profiles/r02/umma_prof_roles.txt). Counted by
+// sampling cfg4's 40 operands: 208 lines per 40 instructions with the mappings above, 99 with
+//  GatherK32: lanes = 32 consecutive K entries of one row (operands gathered along K); the row's
+//             offset is shuffled from the lane that holds it; K chunks 16 bytes apart mod 128 so
+//             the eight 16-byte chunks an instruction writes land on distinct banks
+//  GatherR32: lanes = 32 consecutive rows at one k (operands gathered along their rows); the
+//             K offset is shuffled from the lane that holds it
+template <typename IDX, int CH = kChunk, int ROWS = 128>
+struct GatherK32 {
+  static constexpr int NRW = ROWS / kPW;             // rows per warp
+  static_assert(NRW == 32, "one row per lane of the offset register");
+  IDX rl;                                            // offset of row 32 w + lane
+  uint32_t rv;                                       // row validity, one bit per row of the warp
+  IDX ko;                                            // offset of K entry k0 + lane
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+    const int r = base + NRW * w + l;
+    rl = rtab[r];                                    // tables are padded past the extent
+    rv = __ballot_sync(0xffffffffu, r < extent);
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    ko = __ldg(ktab + k0 + l);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+    const bool kin = k0 + l < K;
+#pragma unroll
+    for (int i = 0; i < NRW; ++i) {
+      const IDX ro = __shfl_sync(0xffffffffu, rl, i);
+      cp_async4(sm + tile_off<CH>(NRW * w + i, l), g + (ro + ko), kin && ((rv >> i) & 1u));
+    }
+  }
+};
+
+template <typename IDX, int CH = kChunk, int ROWS = 128>
+struct GatherR32 {
+  static constexpr int NRW = ROWS / kPW;             // rows per warp
+  static_assert(NRW == 32, "one row per lane");
+  IDX ro;                                            // offset of row 32 w + lane
+  bool rv;
+  IDX kl;                                            // offset of K entry k0 + lane
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+    const int r = base + NRW * w + l;
+    ro = rtab[r];
+    rv = r < extent;
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    kl = __ldg(ktab + k0 + l);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const IDX ko = __shfl_sync(0xffffffffu, kl, k);
+      cp_async4(sm + tile_off<CH>(NRW * w + l, k), g + (ro + ko), rv && k0 + k < K);
+    }
+  }
+};
+
 // operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors,
-// 5 K pairs, 6 row pairs (A)
+// 5 K pairs, 6 row pairs (A), 7 K-run elements one row per instruction, 8 rows one k per
+// instruction
 template <typename IDX, int MODE, int CH = kChunk, int ROWS = 128> struct GatherSel;
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 0, CH, R> { using type = Gather<IDX, false, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 1, CH, R> { using type = Gather<IDX, true, CH, R>; };
@@ -425,6 +494,8 @@ template <typename IDX, int CH, int R> struct GatherSel<IDX, 2, CH, R> { using t
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 3, CH, R> { using type = GatherVM<IDX>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 5, CH, R> { using type = GatherP2K<IDX, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 6, CH, R> { using type = GatherP2M<IDX>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 7, CH, R> { using type = GatherK32<IDX, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 8, CH, R> { using type = GatherR32<IDX, CH, R>; };
 
 #ifdef TC_UMMA_PROF
 // measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
@@ -519,6 +590,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
                    int tiles_m, int tiles_n, double alpha, double beta, Sched sched,
                    int* __restrict__ flags, bool c_lanes_n) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr int kChA = chunk_stride<128 * 4, A_MODE>();
+  constexpr int kChB = chunk_stride<kChunkB - 16, B_MODE>();
   float* stage0 = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * kStage * sizeof(float));
   uint64_t* conv = full + STAGES;
@@ -574,8 +647,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 
   if (warp < kPW) {
     // ---------------------------------- producers ----------------------------------
-    typename GatherSel<IDX, A_MODE>::type ga;
-    typename GatherSel<IDX, B_MODE, kChunkB, kRowsB>::type gb;
+    typename GatherSel<IDX, A_MODE, kChA>::type ga;
+    typename GatherSel<IDX, B_MODE, kChB, kRowsB>::type gb;
     uint32_t it = 0;
     // K offsets depend on the K step only: those of the next step are fetched while this one's
     // copies are in flight, so the table reads stay off the producer's critical path
@@ -617,7 +690,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
           // B: lo rows next to the hi rows of every K chunk
 #pragma unroll
           for (int i = t; i < (BK / 4) * 128; i += kCW * 32) {
-            float4* hi = reinterpret_cast<float4*>(st + kOffBh + (i >> 7) * kChunkB) + (i & 127);
+            float4* hi = reinterpret_cast<float4*>(st + kOffBh + (i >> 7) * kChB) + (i & 127);
             const float4 x = *hi;
             float4 h;
             h.x = tf32_trunc(x.x); h.y = tf32_trunc(x.y); h.z = tf32_trunc(x.z); h.w = tf32_trunc(x.w);
@@ -666,7 +739,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               x = make_float4(st[k * BM + row], st[(k + 1) * BM + row], st[(k + 2) * BM + row],
                               st[(k + 3) * BM + row]);
             } else {
-              x = *reinterpret_cast<const float4*>(st + tile_off(row, k));
+              x = *reinterpret_cast<const float4*>(st + tile_off<kChA>(row, k));
             }
             const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
@@ -914,7 +987,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
             for (int j = 0; j < BK / 8; ++j) {
               const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-              const uint64_t dbh = make_desc<kChunkB>(bh, j), dbl = make_desc<kChunkB>(bl, j);
+              const uint64_t dbh = make_desc<kChB>(bh, j), dbl = make_desc<kChB>(bl, j);
               mma_tf32_ta_pair(d, ah + 8 * j, dbh, idesc, acc0);
               mma_tf32_ta_pair(d, ah + 8 * j, dbl, idesc, 1u);
               mma_tf32_ta_pair(d, al + 8 * j, dbh, idesc, 1u);
@@ -926,7 +999,7 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
             for (int j = 0; j < BK / 8; ++j) {
               const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-              const uint64_t db = make_desc<kChunkB>(bh, j);
+              const uint64_t db = make_desc<kChB>(bh, j);
               mma_tf32_ta(d, ah + 8 * j, db, idesc256, acc0);      // [Ahi.Bhi | Ahi.Blo]
               mma_tf32_ta(d + BN, al + 8 * j, db, idesc, 1u);      // + Alo.Bhi
             }
@@ -937,9 +1010,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
             for (int j = 0; j < BK / 8; ++j) {
               const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-              mma_tf32_ta(d, ah + 8 * j, make_desc(bh, j), idesc, acc0);
-              mma_tf32_ta(d, ah + 8 * j, make_desc(bl, j), idesc, 1u);
-              mma_tf32_ta(d, al + 8 * j, make_desc(bh, j), idesc, 1u);
+              mma_tf32_ta(d, ah + 8 * j, make_desc<kChB>(bh, j), idesc, acc0);
+              mma_tf32_ta(d, ah + 8 * j, make_desc<kChB>(bl, j), idesc, 1u);
+              mma_tf32_ta(d, al + 8 * j, make_desc<kChB>(bh, j), idesc, 1u);
             }
             mma_commit(&aempty[slot]);                 // A slot free once these complete
           } else {
@@ -948,9 +1021,9 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
             for (int j = 0; j < BK / 8; ++j) {
               const uint32_t acc0 = (!chunk_start || j > 0) ? 1u : 0u;
-              mma_tf32(d, make_desc(ah, j), make_desc(bh, j), idesc, acc0);
-              mma_tf32(d, make_desc(ah, j), make_desc(bl, j), idesc, 1u);
-              mma_tf32(d, make_desc(al, j), make_desc(bh, j), idesc, 1u);
+              mma_tf32(d, make_desc<kChA>(ah, j), make_desc<kChB>(bh, j), idesc, acc0);
+              mma_tf32(d, make_desc<kChA>(ah, j), make_desc<kChB>(bl, j), idesc, 1u);
+              mma_tf32(d, make_desc<kChA>(al, j), make_desc<kChB>(bh, j), idesc, 1u);
             }
           }
           if constexpr (kPair) {
@@ -1052,45 +1125,112 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   if (!a.f32 || a.idx64 || a.K < 1) return 0;
   using namespace TC_UMMA_NS;
   // 8-byte pair gathers where the operand's pairs (not all its vectors) are contiguous and
-  // aligned; TC_UMMA_PAIRS=0 turns them off (measurement A/B)
+  // aligned (TC_UMMA_PAIRS=0: off); element gathers one line per instruction (modes 7 / 8;
+  // TC_UMMA_MAP=0: the 4 x 8 / 8 x 4 mappings, modes 1 / 0). Measurement switches, read per call.
   const char* pe2 = getenv("TC_UMMA_PAIRS");
+  const char* pm = getenv("TC_UMMA_MAP");
   const bool pairs = !kPair && !(pe2 && !strcmp(pe2, "0"));
+  // TC_UMMA_MAP (measurement; default "kr"): 'k' = K gathers one row per instruction (both
+  // operands), 'r' = A's row gathers one k per instruction, 'b' = B's as well. Measured on cfg4
+  // (profiles/r02/ab_umma_lines.txt): K gathers +10-32% where the K traversal interleaves
+  // dimensions (cfg4_05, 06, 11), neutral elsewhere; A's row gathers +4-11% (cfg4_04, 07, 18);
+  // B's row gathers -3..-9% on most cases whose B rows are contiguous (the 4-way bank conflicts of
+  // 32 rows at one k in the K-major layout cost more than the lines they save), so off
+  const bool mk = !kPair && (!pm || strchr(pm, 'k'));
+  const bool mr = !kPair && (!pm || strchr(pm, 'r')), mb = !kPair && pm && strchr(pm, 'b');
   const bool a2 = pairs && a.a_vec2_all, b2 = pairs && a.b_vec2_all;
+  const int a_row = mr ? 8 : 0, a_k = mk ? 7 : 1;   // element modes
+  const int b_row = mb ? 8 : 0, b_k = mk ? 7 : 1;
 #ifdef TC_UMMA_ELEM_ONLY
-  const int am = a.a_vec_m ? (a2 ? 6 : 0) : (a2 ? 5 : 1);
-  const int bm = a.b_vec_k ? (b2 ? 5 : 1) : 0;
-  switch (am * 10 + bm) {
+  const int am = a.a_vec_m ? (a2 ? 6 : a_row) : (a2 ? 5 : a_k);
+  const int bm = a.b_vec_k ? (b2 ? 5 : b_k) : b_row;
+  if constexpr (!kPair) {
+    switch (am * 10 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
     case 1: return launch_dir<int, 0, 1>(a, stream);
     case 5: return launch_dir<int, 0, 5>(a, stream);
+    case 7: return launch_dir<int, 0, 7>(a, stream);
+    case 8: return launch_dir<int, 0, 8>(a, stream);
     case 10: return launch_dir<int, 1, 0>(a, stream);
     case 11: return launch_dir<int, 1, 1>(a, stream);
     case 15: return launch_dir<int, 1, 5>(a, stream);
+    case 17: return launch_dir<int, 1, 7>(a, stream);
+    case 18: return launch_dir<int, 1, 8>(a, stream);
     case 50: return launch_dir<int, 5, 0>(a, stream);
     case 51: return launch_dir<int, 5, 1>(a, stream);
     case 55: return launch_dir<int, 5, 5>(a, stream);
+    case 57: return launch_dir<int, 5, 7>(a, stream);
+    case 58: return launch_dir<int, 5, 8>(a, stream);
     case 60: return launch_dir<int, 6, 0>(a, stream);
     case 61: return launch_dir<int, 6, 1>(a, stream);
-    default: return launch_dir<int, 6, 5>(a, stream);
+    case 65: return launch_dir<int, 6, 5>(a, stream);
+    case 67: return launch_dir<int, 6, 7>(a, stream);
+    case 68: return launch_dir<int, 6, 8>(a, stream);
+    case 70: return launch_dir<int, 7, 0>(a, stream);
+    case 71: return launch_dir<int, 7, 1>(a, stream);
+    case 75: return launch_dir<int, 7, 5>(a, stream);
+    case 77: return launch_dir<int, 7, 7>(a, stream);
+    case 78: return launch_dir<int, 7, 8>(a, stream);
+    case 80: return launch_dir<int, 8, 0>(a, stream);
+    case 81: return launch_dir<int, 8, 1>(a, stream);
+    case 85: return launch_dir<int, 8, 5>(a, stream);
+    case 87: return launch_dir<int, 8, 7>(a, stream);
+    default: return launch_dir<int, 8, 8>(a, stream);
+    }
   }
 #else
-  const int am = a.a_vec_m ? (a.a_vec_all ? 3 : (a2 ? 6 : 0)) : (a.a_vec_all ? 2 : (a2 ? 5 : 1));
-  const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : (b2 ? 5 : 1)) : 0;
+  const int am = a.a_vec_m ? (a.a_vec_all ? 3 : (a2 ? 6 : a_row)) : (a.a_vec_all ? 2 : (a2 ? 5 : a_k));
+  const int bm = a.b_vec_k ? (a.b_vec_all ? 2 : (b2 ? 5 : b_k)) : b_row;
   if constexpr (!kPair) {
     switch (am * 10 + bm) {
-      case 5: return launch_dir<int, 0, 5>(a, stream);
-      case 15: return launch_dir<int, 1, 5>(a, stream);
-      case 25: return launch_dir<int, 2, 5>(a, stream);
-      case 35: return launch_dir<int, 3, 5>(a, stream);
-      case 50: return launch_dir<int, 5, 0>(a, stream);
-      case 51: return launch_dir<int, 5, 1>(a, stream);
-      case 52: return launch_dir<int, 5, 2>(a, stream);
-      case 55: return launch_dir<int, 5, 5>(a, stream);
-      case 60: return launch_dir<int, 6, 0>(a, stream);
-      case 61: return launch_dir<int, 6, 1>(a, stream);
-      case 62: return launch_dir<int, 6, 2>(a, stream);
-      case 65: return launch_dir<int, 6, 5>(a, stream);
-      default: break;
+    case 0: return launch_dir<int, 0, 0>(a, stream);
+    case 1: return launch_dir<int, 0, 1>(a, stream);
+    case 2: return launch_dir<int, 0, 2>(a, stream);
+    case 5: return launch_dir<int, 0, 5>(a, stream);
+    case 7: return launch_dir<int, 0, 7>(a, stream);
+    case 8: return launch_dir<int, 0, 8>(a, stream);
+    case 10: return launch_dir<int, 1, 0>(a, stream);
+    case 11: return launch_dir<int, 1, 1>(a, stream);
+    case 12: return launch_dir<int, 1, 2>(a, stream);
+    case 15: return launch_dir<int, 1, 5>(a, stream);
+    case 17: return launch_dir<int, 1, 7>(a, stream);
+    case 18: return launch_dir<int, 1, 8>(a, stream);
+    case 20: return launch_dir<int, 2, 0>(a, stream);
+    case 21: return launch_dir<int, 2, 1>(a, stream);
+    case 22: return launch_dir<int, 2, 2>(a, stream);
+    case 25: return launch_dir<int, 2, 5>(a, stream);
+    case 27: return launch_dir<int, 2, 7>(a, stream);
+    case 28: return launch_dir<int, 2, 8>(a, stream);
+    case 30: return launch_dir<int, 3, 0>(a, stream);
+    case 31: return launch_dir<int, 3, 1>(a, stream);
+    case 32: return launch_dir<int, 3, 2>(a, stream);
+    case 35: return launch_dir<int, 3, 5>(a, stream);
+    case 37: return launch_dir<int, 3, 7>(a, stream);
+    case 38: return launch_dir<int, 3, 8>(a, stream);
+    case 50: return launch_dir<int, 5, 0>(a, stream);
+    case 51: return launch_dir<int, 5, 1>(a, stream);
+    case 52: return launch_dir<int, 5, 2>(a, stream);
+    case 55: return launch_dir<int, 5, 5>(a, stream);
+    case 57: return launch_dir<int, 5, 7>(a, stream);
+    case 58: return launch_dir<int, 5, 8>(a, stream);
+    case 60: return launch_dir<int, 6, 0>(a, stream);
+    case 61: return launch_dir<int, 6, 1>(a, stream);
+    case 62: return launch_dir<int, 6, 2>(a, stream);
+    case 65: return launch_dir<int, 6, 5>(a, stream);
+    case 67: return launch_dir<int, 6, 7>(a, stream);
+    case 68: return launch_dir<int, 6, 8>(a, stream);
+    case 70: return launch_dir<int, 7, 0>(a, stream);
+    case 71: return launch_dir<int, 7, 1>(a, stream);
+    case 72: return launch_dir<int, 7, 2>(a, stream);
+    case 75: return launch_dir<int, 7, 5>(a, stream);
+    case 77: return launch_dir<int, 7, 7>(a, stream);
+    case 78: return launch_dir<int, 7, 8>(a, stream);
+    case 80: return launch_dir<int, 8, 0>(a, stream);
+    case 81: return launch_dir<int, 8, 1>(a, stream);
+    case 82: return launch_dir<int, 8, 2>(a, stream);
+    case 85: return launch_dir<int, 8, 5>(a, stream);
+    case 87: return launch_dir<int, 8, 7>(a, stream);
+    default: return launch_dir<int, 8, 8>(a, stream);
     }
   }
   switch (am * 10 + bm) {
