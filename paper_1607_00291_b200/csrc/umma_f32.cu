@@ -135,7 +135,9 @@ constexpr int kChunk = 128 * 4 + 16;
 // K chunk stride of an operand's staging (floats): the one-row-per-instruction K gather (mode 7)
 // writes eight consecutive chunks per instruction, which a 64-byte pad would put on two bank
 // groups; a 16-byte pad spreads them over all banks
-template <int BASE, int MODE> constexpr int chunk_stride() { return BASE + (MODE == 7 ? 4 : 16); }
+template <int BASE, int MODE> constexpr int chunk_stride() {
+  return BASE + ((MODE == 7 || MODE == 5) ? 4 : 16);
+}
 template <int CH = kChunk>
 __device__ __forceinline__ int tile_off(int r, int k) {
   return (k >> 2) * CH + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
@@ -350,40 +352,39 @@ struct GatherVM {
 // qualify against 17), half the copy instructions of the element gathers -- the producers of the
 // element-gather cases issue one 4-byte cp.async per element and are bound by that (~8 cycles
 // each, profiles/r02/umma_prof_roles.txt).
-//  GatherP2K: pairs along K (4 consecutive... lanes = 4 rows x 8 pairs = 16 consecutive k) into
-//             the K-major staging layout (a pair never straddles a core-matrix row)
+//  GatherP2K: pairs along K into the K-major staging layout (a pair never straddles a
+//             core-matrix row)
 //  GatherP2M: pairs along the rows (A only) into the [k][m] staging of GatherVM; lanes = 32 pairs
 //             = 64 consecutive m at one k
 template <typename IDX, int CH = kChunk, int ROWS = 128>
 struct GatherP2K {
-  static constexpr int NR = ROWS / 4 / kPW;          // row groups of 4 per warp
-  IDX ro[NR];
+  // lanes = 2 rows x 16 pairs (all 32 K of a step): two 128-byte lines per instruction when
+  // the rows' K runs are contiguous (4 rows x 8 pairs touched four); K chunks 16 bytes apart
+  // mod 128 (chunk_stride), so the eight chunks of a row land on distinct banks. The warp's 32
+  // row offsets live one per lane and are shuffled to the instruction that needs them.
+  static constexpr int NRW = ROWS / kPW;             // rows per warp
+  static_assert(NRW == 32, "one row offset per lane");
+  IDX rl;
   uint32_t rv;
-  IDX ko[2];
-  __device__ __forceinline__ static int row(int w, int i, int l) { return 4 * (w * NR + i) + (l >> 3); }
+  IDX ko;
   __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
                                        int l) {
-    rv = 0;
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const int r = base + row(w, i, l);
-      ro[i] = rtab[r];
-      rv |= (r < extent ? 1u : 0u) << i;
-    }
+    const int r = base + NRW * w + l;
+    rl = rtab[r];
+    rv = __ballot_sync(0xffffffffu, r < extent);
   }
   __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) ko[h] = __ldg(ktab + k0 + 16 * h + 2 * (l & 7));
+    ko = __ldg(ktab + k0 + 2 * (l & 15));
   }
   __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
                                         int l) {
+    const int kk = 2 * (l & 15);
+    const bool kin = k0 + kk < K;                    // K is even here
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int kk = 16 * h + 2 * (l & 7);
-      const bool kin = k0 + kk < K;                  // K is even here
-#pragma unroll
-      for (int i = 0; i < NR; ++i)
-        cp_async8(sm + tile_off<CH>(row(w, i, l), kk), g + (ro[i] + ko[h]), kin && ((rv >> i) & 1u));
+    for (int i = 0; i < NRW / 2; ++i) {
+      const int r = 2 * i + (l >> 4);
+      const IDX ro = __shfl_sync(0xffffffffu, rl, r);
+      cp_async8(sm + tile_off<CH>(NRW * w + r, kk), g + (ro + ko), kin && ((rv >> r) & 1u));
     }
   }
 };
