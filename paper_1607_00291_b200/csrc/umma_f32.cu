@@ -135,6 +135,8 @@ constexpr int kChunk = 128 * 4 + 16;
 // K chunk stride of an operand's staging (floats): the one-row-per-instruction K gather (mode 7)
 // writes eight consecutive chunks per instruction, which a 64-byte pad would put on two bank
 // groups; a 16-byte pad spreads them over all banks
+// (the same pad under the 16-byte K-vector gathers, mode 2, removes their bank conflicts but
+// measured 1% slower over cfg4: profiles/r02/ab_umma_vkpad.txt)
 template <int BASE, int MODE> constexpr int chunk_stride() {
   return BASE + ((MODE == 7 || MODE == 5) ? 4 : 16);
 }
