@@ -406,12 +406,18 @@ static Piece piece_of(const tc_tensor* T, int pos, int64_t x0, int64_t len) {
   return p;
 }
 
-constexpr int kHostChunks = 8;
+// chunks of the host path: 8 (TC_HOST_CHUNKS overrides, measurement)
+static int host_chunks() {
+  const char* e = getenv("TC_HOST_CHUNKS");
+  const int n = e ? atoi(e) : 8;
+  return n < 1 ? 1 : (n > 64 ? 64 : n);
+}
 constexpr int64_t kHostChunkMinBytes = 64ll << 20;
 
 static int contract_host(tc_dtype dtype, double alpha, const tc_tensor* A, const tc_tensor* B,
                          double beta, const tc_tensor* C, cudaStream_t s) {
   Nvtx range("tc_contract_host");
+  const int kHostChunks = host_chunks();
   std::shared_ptr<Plan> full;
   int rc = get_plan(dtype, A, B, C, &full);
   if (rc != TC_OK) return rc;
