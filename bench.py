@@ -39,9 +39,10 @@ import workloads as W  # noqa: E402
 SHARD_LABELS = "abc"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "PEAKS_FP64.json")
 # DRAM bytes per launch of the contraction kernel on the full cfg5 workload, from
-# `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum` of this same
-# command (tools/gpu/r01_checkpoint.sh); the counters of the `--set full` memory section.
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01", "traffic_cfg5_full.csv")
+# `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum` of this same
+# command (tools/gpu/r02_evidence.sh, the round-2 launch list); the counters of the `--set full`
+# memory section.
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02", "launches_bench_r02.csv")
 
 
 def ncu_traffic(path, kernel_prefix="tc_dmma_ws_kernel"):
@@ -451,7 +452,7 @@ def run_native(args):
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
                      "traffic": None if args.small or world > 1 else ncu_traffic(TRAFFIC_FILE),
                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, one "
-                                       "launch of this workload (profiles/r01/traffic_cfg5_full.csv)",
+                                       "launch of this workload (profiles/r02/launches_bench_r02.csv)",
                      "peak_source": "profiles/PEAKS_FP64.json dmma_tflops (measured DMMA.8x8x4 "
                                     "loop on this pool's B200; fp64 has no entry in "
                                     "MEASURED_PEAKS.json)",
