@@ -297,7 +297,7 @@ static int launch_t(const Args& p, int num_sms, cudaStream_t s) {
   // of the column blocks
   static const int occ2 = [] {
     const char* e = getenv("TC_RANKK_OCC2");
-    return e ? atoi(e) : 32;
+    return e ? atoi(e) : 64;
   }();
   long long gy = ((long long)(v1 ? TC_RANKK_OCC : occ2) * num_sms + gx - 1) / gx;
   if (gy > nblocks) gy = nblocks;
