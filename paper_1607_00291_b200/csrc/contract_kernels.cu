@@ -414,10 +414,14 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (choice == 1 && !args.f32)
     return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
   if (choice == 0 && args.f32 && umma_f32_enabled()) {
-    // N = 256 form when neither operand has 16-byte vector gathers (TC_UMMA_FORM=128|256 forces)
+    // N = 256 form (element, pair and one-line gathers; TC_UMMA_FORM=128|256 forces) unless A
+    // takes the 16-byte M-vector gathers into its [k][m] staging: since the round-2 gather modes
+    // the N = 256 form wins on 15 of cfg4's 20 cases (cfg4_09 110 -> 153, cfg4_02 83 -> 98
+    // TF/s) and loses on the M-vector ones (cfg4_00 115 -> 106, cfg4_13 133 -> 124;
+    // profiles/r02/ab_umma_forms2.txt)
     const char* fe = getenv("TC_UMMA_FORM");
-    const bool vec = args.a_vec_all || (args.b_vec_k && args.b_vec_all);
-    const bool n256 = fe ? !strcmp(fe, "256") : !vec;
+    const bool a_mvec = args.a_vec_m && args.a_vec_all;
+    const bool n256 = fe ? !strcmp(fe, "256") : !a_mvec;
     const bool pair = fe && !strcmp(fe, "pair");
     const int r = pair   ? launch_umma_f32_pair(args, stream)
                   : n256 ? launch_umma_f32_n256(args, stream)
