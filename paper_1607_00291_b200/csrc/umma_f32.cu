@@ -487,6 +487,48 @@ struct GatherR32 {
   }
 };
 
+// B gathered along N with 16-byte vectors / 8-byte pairs (N = 256 form only, modes 10 / 11): B's
+// K-major layout keeps consecutive n 16 bytes apart, so N vectors cannot land in it directly;
+// they go to a [k][n] staging that occupies the lo half of each K chunk (rows 128-255 x 4 K =
+// 512 floats, the same size), and the converter warps move them into the hi rows and write the
+// lo rows over the staging (all values read into registers first). A quarter (vectors) or half
+// (pairs) of the element gathers' copy instructions for B (19 of cfg4's 40 operands have N pairs).
+template <typename IDX, int CH, int VEC>
+struct GatherVN {
+  static constexpr int KPW = BK / kPW;               // k rows per warp (8)
+  static constexpr int NPL = 32 * VEC;               // n per warp instruction (128 / 64)
+  IDX ro[128 / NPL];
+  bool rv[128 / NPL];
+  IDX ko[KPW];
+  __device__ __forceinline__ void init(const IDX* __restrict__ rtab, int base, int extent, int w,
+                                       int l) {
+#pragma unroll
+    for (int h = 0; h < 128 / NPL; ++h) {
+      const int r = base + NPL * h + VEC * l;
+      ro[h] = rtab[r];
+      rv[h] = r < extent;                            // N is a multiple of VEC here
+    }
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    const int w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < KPW; ++j) ko[j] = __ldg(ktab + k0 + w * KPW + j);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int j = 0; j < KPW; ++j) {
+      const int k = w * KPW + j;
+      float* row = sm + (k >> 2) * CH + 512 + (k & 3) * 128;
+#pragma unroll
+      for (int h = 0; h < 128 / NPL; ++h) {
+        if constexpr (VEC == 4) cp_async16(row + NPL * h + 4 * l, g + (ro[h] + ko[j]), rv[h] && k0 + k < K);
+        else cp_async8(row + NPL * h + 2 * l, g + (ro[h] + ko[j]), rv[h] && k0 + k < K);
+      }
+    }
+  }
+};
+
 // operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors,
 // 5 K pairs, 6 row pairs (A), 7 K-run elements one row per instruction, 8 rows one k per
 // instruction
@@ -499,6 +541,8 @@ template <typename IDX, int CH, int R> struct GatherSel<IDX, 5, CH, R> { using t
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 6, CH, R> { using type = GatherP2M<IDX>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 7, CH, R> { using type = GatherK32<IDX, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 8, CH, R> { using type = GatherR32<IDX, CH, R>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 10, CH, R> { using type = GatherVN<IDX, CH, 4>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 11, CH, R> { using type = GatherVN<IDX, CH, 2>; };
 
 #ifdef TC_UMMA_PROF
 // measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
@@ -689,7 +733,26 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
         const int s = it % STAGES;
         PWAIT(1, mbar_wait(&full[s], (it / STAGES) & 1));
         float* st = stage0 + s * kStage;
-        if constexpr (kN256) {
+        if constexpr (kN256 && (B_MODE == 10 || B_MODE == 11)) {
+          // B from the [k][n] staging in the lo halves: this thread's row n, all 32 K values
+          // into registers, then (once every converter thread has read) the hi rows and the lo
+          // rows over the staging
+          static_assert(kCW == 4, "one converter thread per B row");
+          float v[BK];
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[4 * c + j] = st[kOffBh + c * kChB + 512 + j * 128 + t];
+          asm volatile("bar.sync 3, %0;\n" ::"n"(kCW * 32) : "memory");   // converters only
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            const float4 x = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            float4* hi = reinterpret_cast<float4*>(st + kOffBh + c * kChB) + t;
+            *hi = x;
+            hi[128] = make_float4(lo_round(x.x - tf32_trunc(x.x)), lo_round(x.y - tf32_trunc(x.y)),
+                                  lo_round(x.z - tf32_trunc(x.z)), lo_round(x.w - tf32_trunc(x.w)));
+          }
+        } else if constexpr (kN256) {
           // B: lo rows next to the hi rows of every K chunk
 #pragma unroll
           for (int i = t; i < (BK / 4) * 128; i += kCW * 32) {
@@ -1145,39 +1208,54 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   const int a_row = mr ? 8 : 0, a_k = mk ? 7 : 1;   // element modes
   const int b_row = mb ? 8 : 0, b_k = mk ? 7 : 1;
 #ifdef TC_UMMA_ELEM_ONLY
+  // TC_UMMA_BN=0: B along N by elements even where its N vectors / pairs qualify (measurement)
+  const char* pbn = getenv("TC_UMMA_BN");
+  const bool bn = !(pbn && !strcmp(pbn, "0"));
   const int am = a.a_vec_m ? (a2 ? 6 : a_row) : (a2 ? 5 : a_k);
-  const int bm = a.b_vec_k ? (b2 ? 5 : b_k) : b_row;
+  const int bm = a.b_vec_k ? (b2 ? 5 : b_k) : (bn && a.b_vec_all ? 10 : (bn && b2 ? 11 : b_row));
   if constexpr (!kPair) {
-    switch (am * 10 + bm) {
+    switch (am * 100 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
     case 1: return launch_dir<int, 0, 1>(a, stream);
     case 5: return launch_dir<int, 0, 5>(a, stream);
     case 7: return launch_dir<int, 0, 7>(a, stream);
     case 8: return launch_dir<int, 0, 8>(a, stream);
-    case 10: return launch_dir<int, 1, 0>(a, stream);
-    case 11: return launch_dir<int, 1, 1>(a, stream);
-    case 15: return launch_dir<int, 1, 5>(a, stream);
-    case 17: return launch_dir<int, 1, 7>(a, stream);
-    case 18: return launch_dir<int, 1, 8>(a, stream);
-    case 50: return launch_dir<int, 5, 0>(a, stream);
-    case 51: return launch_dir<int, 5, 1>(a, stream);
-    case 55: return launch_dir<int, 5, 5>(a, stream);
-    case 57: return launch_dir<int, 5, 7>(a, stream);
-    case 58: return launch_dir<int, 5, 8>(a, stream);
-    case 60: return launch_dir<int, 6, 0>(a, stream);
-    case 61: return launch_dir<int, 6, 1>(a, stream);
-    case 65: return launch_dir<int, 6, 5>(a, stream);
-    case 67: return launch_dir<int, 6, 7>(a, stream);
-    case 68: return launch_dir<int, 6, 8>(a, stream);
-    case 70: return launch_dir<int, 7, 0>(a, stream);
-    case 71: return launch_dir<int, 7, 1>(a, stream);
-    case 75: return launch_dir<int, 7, 5>(a, stream);
-    case 77: return launch_dir<int, 7, 7>(a, stream);
-    case 78: return launch_dir<int, 7, 8>(a, stream);
-    case 80: return launch_dir<int, 8, 0>(a, stream);
-    case 81: return launch_dir<int, 8, 1>(a, stream);
-    case 85: return launch_dir<int, 8, 5>(a, stream);
-    case 87: return launch_dir<int, 8, 7>(a, stream);
+    case 100: return launch_dir<int, 1, 0>(a, stream);
+    case 101: return launch_dir<int, 1, 1>(a, stream);
+    case 105: return launch_dir<int, 1, 5>(a, stream);
+    case 107: return launch_dir<int, 1, 7>(a, stream);
+    case 108: return launch_dir<int, 1, 8>(a, stream);
+    case 500: return launch_dir<int, 5, 0>(a, stream);
+    case 501: return launch_dir<int, 5, 1>(a, stream);
+    case 505: return launch_dir<int, 5, 5>(a, stream);
+    case 507: return launch_dir<int, 5, 7>(a, stream);
+    case 508: return launch_dir<int, 5, 8>(a, stream);
+    case 600: return launch_dir<int, 6, 0>(a, stream);
+    case 601: return launch_dir<int, 6, 1>(a, stream);
+    case 605: return launch_dir<int, 6, 5>(a, stream);
+    case 607: return launch_dir<int, 6, 7>(a, stream);
+    case 608: return launch_dir<int, 6, 8>(a, stream);
+    case 700: return launch_dir<int, 7, 0>(a, stream);
+    case 701: return launch_dir<int, 7, 1>(a, stream);
+    case 705: return launch_dir<int, 7, 5>(a, stream);
+    case 707: return launch_dir<int, 7, 7>(a, stream);
+    case 708: return launch_dir<int, 7, 8>(a, stream);
+    case 800: return launch_dir<int, 8, 0>(a, stream);
+    case 801: return launch_dir<int, 8, 1>(a, stream);
+    case 805: return launch_dir<int, 8, 5>(a, stream);
+    case 807: return launch_dir<int, 8, 7>(a, stream);
+    case 10: return launch_dir<int, 0, 10>(a, stream);
+    case 11: return launch_dir<int, 0, 11>(a, stream);
+    case 110: return launch_dir<int, 1, 10>(a, stream);
+    case 111: return launch_dir<int, 1, 11>(a, stream);
+    case 510: return launch_dir<int, 5, 10>(a, stream);
+    case 511: return launch_dir<int, 5, 11>(a, stream);
+    case 610: return launch_dir<int, 6, 10>(a, stream);
+    case 611: return launch_dir<int, 6, 11>(a, stream);
+    case 710: return launch_dir<int, 7, 10>(a, stream);
+    case 711: return launch_dir<int, 7, 11>(a, stream);
+    case 810: return launch_dir<int, 8, 10>(a, stream);
+    case 811: return launch_dir<int, 8, 11>(a, stream);
     default: return launch_dir<int, 8, 8>(a, stream);
     }
   }
