@@ -414,14 +414,12 @@ int launch_contract(const LaunchArgs& args, cudaStream_t stream) {
   if (choice == 1 && !args.f32)
     return args.idx64 ? dispatch_dir<long long>(args, stream) : dispatch_dir<int>(args, stream);
   if (choice == 0 && args.f32 && umma_f32_enabled()) {
-    // N = 256 form (element, pair and one-line gathers; TC_UMMA_FORM=128|256 forces) unless A
-    // takes the 16-byte M-vector gathers into its [k][m] staging: since the round-2 gather modes
-    // the N = 256 form wins on 15 of cfg4's 20 cases (cfg4_09 110 -> 153, cfg4_02 83 -> 98
-    // TF/s) and loses on the M-vector ones (cfg4_00 115 -> 106, cfg4_13 133 -> 124;
-    // profiles/r02/ab_umma_forms2.txt)
+    // N = 256 form by default (TC_UMMA_FORM=128|256|pair forces a form): with the round-2
+    // gather modes (one-line element gathers, pairs, B's N vectors through a [k][n] staging, A's
+    // M vectors) it wins on every cfg4 case and on the GEMM-layout sweep (4096^3 141 -> 156
+    // TF/s; profiles/r02/ab_umma_forms2.txt, ab_umma_am.txt)
     const char* fe = getenv("TC_UMMA_FORM");
-    const bool a_mvec = args.a_vec_m && args.a_vec_all;
-    const bool n256 = fe ? !strcmp(fe, "256") : !a_mvec;
+    const bool n256 = fe ? !strcmp(fe, "256") : true;
     const bool pair = fe && !strcmp(fe, "pair");
     const int r = pair   ? launch_umma_f32_pair(args, stream)
                   : n256 ? launch_umma_f32_n256(args, stream)

@@ -1211,8 +1211,16 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   // TC_UMMA_BN=0: B along N by elements even where its N vectors / pairs qualify (measurement)
   const char* pbn = getenv("TC_UMMA_BN");
   const bool bn = !(pbn && !strcmp(pbn, "0"));
-  const int am = a.a_vec_m ? (a2 ? 6 : a_row) : (a2 ? 5 : a_k);
-  const int bm = a.b_vec_k ? (b2 ? 5 : b_k) : (bn && a.b_vec_all ? 10 : (bn && b2 ? 11 : b_row));
+  // TC_UMMA_AM=0: no 16-byte M vectors for A in this form (measurement)
+  const char* pam = getenv("TC_UMMA_AM");
+  const bool amv = !(pam && !strcmp(pam, "0"));
+  // TC_UMMA_KV=1: 16-byte K vectors (mode 2) in this form too (measurement)
+  const char* pkv = getenv("TC_UMMA_KV");
+  const bool kv = pkv && !strcmp(pkv, "1");
+  const int am = a.a_vec_m ? (amv && a.a_vec_all ? 3 : (a2 ? 6 : a_row))
+                           : (kv && a.a_vec_all ? 2 : (a2 ? 5 : a_k));
+  const int bm = a.b_vec_k ? (kv && a.b_vec_all ? 2 : (b2 ? 5 : b_k))
+                           : (bn && a.b_vec_all ? 10 : (bn && b2 ? 11 : b_row));
   if constexpr (!kPair) {
     switch (am * 100 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
@@ -1256,6 +1264,28 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
     case 711: return launch_dir<int, 7, 11>(a, stream);
     case 810: return launch_dir<int, 8, 10>(a, stream);
     case 811: return launch_dir<int, 8, 11>(a, stream);
+    case 300: return launch_dir<int, 3, 0>(a, stream);
+    case 301: return launch_dir<int, 3, 1>(a, stream);
+    case 305: return launch_dir<int, 3, 5>(a, stream);
+    case 307: return launch_dir<int, 3, 7>(a, stream);
+    case 308: return launch_dir<int, 3, 8>(a, stream);
+    case 310: return launch_dir<int, 3, 10>(a, stream);
+    case 311: return launch_dir<int, 3, 11>(a, stream);
+    case 2: return launch_dir<int, 0, 2>(a, stream);
+    case 102: return launch_dir<int, 1, 2>(a, stream);
+    case 200: return launch_dir<int, 2, 0>(a, stream);
+    case 201: return launch_dir<int, 2, 1>(a, stream);
+    case 202: return launch_dir<int, 2, 2>(a, stream);
+    case 205: return launch_dir<int, 2, 5>(a, stream);
+    case 207: return launch_dir<int, 2, 7>(a, stream);
+    case 208: return launch_dir<int, 2, 8>(a, stream);
+    case 210: return launch_dir<int, 2, 10>(a, stream);
+    case 211: return launch_dir<int, 2, 11>(a, stream);
+    case 302: return launch_dir<int, 3, 2>(a, stream);
+    case 502: return launch_dir<int, 5, 2>(a, stream);
+    case 602: return launch_dir<int, 6, 2>(a, stream);
+    case 702: return launch_dir<int, 7, 2>(a, stream);
+    case 802: return launch_dir<int, 8, 2>(a, stream);
     default: return launch_dir<int, 8, 8>(a, stream);
     }
   }
