@@ -5,8 +5,10 @@
 // in shared memory for the whole kernel. The general 128 x 128 tile would spend most of its
 // DMMA work on padding and restart its pipeline every 2-5 K steps.
 //
-// Persistent CTAs (one per SM, 256 threads) each load Y once (gathered through its scatter
-// vectors), then walk 64-row blocks of X: a 3-deep ring of X blocks is gathered
+// Two forms. For NP, KP <= 32 (the HBM-bound class) a warp-specialised kernel (producer warps,
+// an mbarrier ring, consumer warps; tc_skinny_ws_kernel below). Otherwise:
+// Persistent CTAs (256 threads) each load Y once (gathered through its scatter
+// vectors), then walk 64-row blocks of X: a 2-3-deep ring of X blocks is gathered
 // with cp.async (coalesced element copies along X's unit-stride direction, written to the
 // [k][row] layout), each block is multiplied on the FP64 tensor cores (mma.sync m16n8k4 f64 ->
 // DMMA.8x8x4; 8 warps = 4 row groups x 2 column halves) and written through the scatter
@@ -33,6 +35,7 @@ constexpr int kMaxN = 96;           // small free extent (padded to a multiple o
 constexpr int kMaxK = 80;           // bound extent (padded to a multiple of 4)
 constexpr int kBufs = 3;            // X ring depth
 constexpr int kXP = kRows + 4;      // [k][row] pitch (doubles): conflict-free fragment loads
+constexpr int kXPSkew = kRows + 20; // pitch with a skewed row layout (Args::sw > 0), = 4 (mod 16)
 
 struct Args {
   const double* X;
@@ -47,23 +50,27 @@ struct Args {
   int R, NC, K;     // long extent, small extent, bound extent
   int NP, KP;       // NC rounded up to 16, K rounded up to 4
   int bu, bv;       // X rows come in bv runs of bu contiguous elements (plan.cpp); 1, 1: plain
+  int xp, sw;       // X ring pitch (doubles) and row skew: block row r sits at r + sw (r / 16)
+  int dbg;          // measurement only (TC_SKINNY_DBG): 1 skip the MMA, 2 the X loads, 4 the stores
   double alpha, beta;
 };
 
+// wr: the warp's first row position in the ring buffer (16 rows, contiguous), xp its pitch
 template <typename IDX, int NW>   // NW: n8 blocks per warp (NP / 16)
-__device__ __forceinline__ void block_mma(const double* xs, const double* ys, int yp, int KP,
-                                          int wr, int wc, int g, int t, double (&acc)[NW][4]) {
+__device__ __forceinline__ void block_mma(const double* xs, int xp, const double* ys, int yp,
+                                          int KP, int wr, int wc, int g, int t,
+                                          double (&acc)[NW][4]) {
 #pragma unroll
   for (int j = 0; j < NW; ++j)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[j][q] = 0.0;
   // fragments of step k4 + 4 load while step k4 multiplies (KP is a multiple of 4)
-  double a0 = xs[t * kXP + wr + g], a1 = xs[t * kXP + wr + g + 8], b[NW];
+  double a0 = xs[t * xp + wr + g], a1 = xs[t * xp + wr + g + 8], b[NW];
 #pragma unroll
   for (int j = 0; j < NW; ++j) b[j] = ys[t * yp + wc + 8 * j + g];
   for (int k4 = 0; k4 < KP; k4 += 4) {
     const int kn = k4 + 4 < KP ? k4 + 4 : k4;
-    const double na0 = xs[(kn + t) * kXP + wr + g], na1 = xs[(kn + t) * kXP + wr + g + 8];
+    const double na0 = xs[(kn + t) * xp + wr + g], na1 = xs[(kn + t) * xp + wr + g + 8];
     double nb[NW];
 #pragma unroll
     for (int j = 0; j < NW; ++j) nb[j] = ys[(kn + t) * yp + wc + 8 * j + g];
@@ -78,15 +85,19 @@ __device__ __forceinline__ void block_mma(const double* xs, const double* ys, in
 
 // ROWS_UNIT: X is contiguous along its rows (lanes take consecutive rows); otherwise along K
 // (lanes take 8 consecutive K entries of 4 rows).
+#ifndef TC_SKINNY_MINB
+#define TC_SKINNY_MINB 1   // experiment: -DTC_SKINNY_MINB=3 caps registers for 3 CTAs per SM
+#endif
 template <typename IDX, bool ROWS_UNIT, int NW, int kBufs>
-__global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
+__global__ void __launch_bounds__(kThreads, TC_SKINNY_MINB) tc_skinny_kernel(Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int yp = a.NP + 4;   // [k][col] pitch of Y (doubles), = 8 (mod 16) words per row
   double* ys = reinterpret_cast<double*>(smem_raw);
   double* xs = ys + a.KP * yp;
   // X's K offsets and C's small-bundle offsets, once per CTA (read from shared memory by the
   // loader and the epilogue instead of a dependent global load per copy / store)
-  IDX* xks = reinterpret_cast<IDX*>(xs + kBufs * a.KP * kXP);
+  const int xp = a.xp;
+  IDX* xks = reinterpret_cast<IDX*>(xs + kBufs * a.KP * xp);
   IDX* ccs = xks + a.KP;
   const IDX* xr = static_cast<const IDX*>(a.xr);
   const IDX* xk = static_cast<const IDX*>(a.xk);
@@ -112,7 +123,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
   // + (lane >> 3)). Their offsets are fetched one block ahead (rows()), so the loader never
   // waits on the row table when it issues the copies (issue()).
   const int bb = a.bu * a.bv;
-  int rl[2];
+  int rl[2], pl[2];   // block row, and its position in the ring buffer (skewed)
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if constexpr (ROWS_UNIT) {
@@ -123,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
     } else {
       rl[h] = 4 * warp + 32 * h + (lane >> 3);
     }
+    pl[h] = rl[h] + a.sw * (rl[h] >> 4);
   }
   // (strides may be negative, so validity travels in rv, not in the offset)
   auto rows = [&](int blk, IDX (&ro)[2], bool (&rv)[2]) {
@@ -134,7 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
     }
   };
   auto issue = [&](int buf, const IDX (&ro)[2], const bool (&rv)[2]) {
-    double* d = xs + buf * (a.KP * kXP);
+    if (a.dbg & 2) return;
+    double* d = xs + buf * (a.KP * xp);
     if constexpr (ROWS_UNIT) {
 #pragma unroll 4
       for (int k = warp; k < a.KP; k += kThreads / 32) {
@@ -142,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
         const IDX ko = xks[k];
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          cp_async8(d + k * kXP + rl[h], a.X + (ro[h] + ko), kin && rv[h]);
+          cp_async8(d + k * xp + pl[h], a.X + (ro[h] + ko), kin && rv[h]);
       }
     } else {
       const int kk = lane & 7;
@@ -153,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
           const IDX ko = xks[k];
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            cp_async8(d + k * kXP + rl[h], a.X + (ro[h] + ko), rv[h] && k < a.K);
+            cp_async8(d + k * xp + pl[h], a.X + (ro[h] + ko), rv[h] && k < a.K);
         }
       }
     }
@@ -192,7 +205,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
     rows(blockIdx.x + (it + kBufs) * gridDim.x, ro, rv);
     cp_async_wait<kBufs - 1>();
     __syncthreads();
-    block_mma<IDX, NW>(xs + (it % kBufs) * (a.KP * kXP), ys, yp, a.KP, wr, wc, g, t, acc);
+    if (!(a.dbg & 1)) {
+      block_mma<IDX, NW>(xs + (it % kBufs) * (a.KP * xp), xp, ys, yp, a.KP,
+                         wr + a.sw * (wr >> 4), wc, g, t, acc);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NW; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[j][q] = xs[(it % kBufs) * (a.KP * xp) + q * xp + wr + g];
+    }
+    if (a.dbg & 4) { __syncthreads(); continue; }
     // epilogue: rows wr + g (+8), columns wc + 8 j + 2 t (+1). A full block with every column
     // in range and beta == 0 stores without checks (the streaming case this kernel is for).
     if (a.beta == 0.0 && cr0 + 8 < a.R && a.NC == a.NP) {
@@ -227,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_skinny_kernel(Args a) {
 
 template <typename IDX, bool ROWS_UNIT, int NW, int NBUF>
 static int launch_nb(const Args& a, int nsm, cudaStream_t s) {
-  const int smem = (a.KP * (a.NP + 4) + NBUF * a.KP * kXP) * (int)sizeof(double) +
+  const int smem = (a.KP * (a.NP + 4) + NBUF * a.KP * a.xp) * (int)sizeof(double) +
                    (a.KP + a.NP) * (int)sizeof(IDX);
   auto kern = tc_skinny_kernel<IDX, ROWS_UNIT, NW, NBUF>;
   static std::atomic<int> attr[kMaxDevices];
@@ -262,8 +284,251 @@ static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
   return launch_nb<IDX, ROWS_UNIT, NW, kBufs>(a, nsm, s);
 }
 
+// ---- warp-specialised form (the HBM-bound class: NP <= 32, KP <= 32) -------------------------
+// The synchronous kernel above loads a block, waits, multiplies, stores: per SM at most two
+// blocks are in flight and the DMMA pipe idles while a CTA waits (f2_00: X loads alone 66 us,
+// stores alone 81 us, MMA alone 83 us, all three 137 us; profiles/r02/ab_skinny_ws.txt). Here one
+// persistent CTA per SM splits the roles: kWsProd producer warps gather X blocks into an S-deep
+// ring (cp.async, completion tracked by an mbarrier per stage), and CG groups of 8 consumer warps
+// multiply (Y held in registers for the CTA's lifetime), release the stage, and store C from
+// registers. Up to S - 1 blocks per SM are in flight while the consumers compute.
+constexpr int kWsProd = 4;
+constexpr int kWsMaxK4 = 8;   // KP <= 32
+constexpr int kWsAhead = 4;   // producer: row-offset lookahead (blocks)
+
+template <typename IDX, bool ROWS_UNIT, int NW, int CG>
+__global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kernel(Args a, int S) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int yp = a.NP + 4, xp = a.xp, stage = a.KP * xp;
+  double* ys = reinterpret_cast<double*>(smem_raw);
+  double* xs = ys + a.KP * yp;
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs + S * stage);
+  uint64_t* empty = full + S;
+  IDX* xks = reinterpret_cast<IDX*>(empty + S);
+  IDX* ccs = xks + a.KP;
+  const IDX* xr = static_cast<const IDX*>(a.xr);
+  const IDX* xk = static_cast<const IDX*>(a.xk);
+  const IDX* yk = static_cast<const IDX*>(a.yk);
+  const IDX* yc = static_cast<const IDX*>(a.yc);
+  const IDX* cr = static_cast<const IDX*>(a.cr);
+  const int nt = 32 * (kWsProd + 8 * CG);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int k = tid; k < a.KP; k += nt) xks[k] = k < a.K ? xk[k] : 0;
+  for (int n = tid; n < a.NP; n += nt) ccs[n] = n < a.NC ? static_cast<const IDX*>(a.cc)[n] : 0;
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) {
+      mbar_init(&full[q], kWsProd * 32);   // one cp.async completion arrival per producer thread
+      mbar_init(&empty[q], 8);             // one arrival per consumer warp of the group
+    }
+  }
+  for (int e = tid; e < a.KP * a.NP; e += nt) {   // Y, once (zero outside K x NC)
+    const int k = e / a.NP, n = e - k * a.NP;
+    const bool in = k < a.K && n < a.NC;
+    cp_async8(ys + k * yp + n, a.Y + (in ? yk[k] + yc[n] : 0), in);
+  }
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+
+  const int nblk = (a.R + kRows - 1) / kRows;
+  if (warp < kWsProd) {
+    // ---- producers: rows-unit lanes take rows 32 h + lane (sub-divided as in the synchronous
+    // kernel) for K rows warp, warp + 4, ..; K-unit lanes take 8 consecutive K entries of rows
+    // (lane >> 3) + 4 warp + 16 h.
+    constexpr int H = ROWS_UNIT ? 2 : 4;
+    const int bb = a.bu * a.bv;
+    int rl[H], pl[H];
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      if constexpr (ROWS_UNIT) {
+        const int e = 32 * h + lane;
+        rl[h] = (e % a.bu) * a.bv + (e / a.bu) % a.bv + (e / bb) * bb;
+      } else {
+        rl[h] = (lane >> 3) + 4 * warp + 16 * h;
+      }
+      pl[h] = rl[h] + a.sw * (rl[h] >> 4);
+    }
+    // the row offsets of a block are fetched kWsAhead blocks before its copies are issued
+    // (a register ring; the loop is unrolled by kWsAhead so the ring is statically indexed):
+    // the producer's own iteration is short, a one-block lookahead would expose the table's
+    // load latency on every block
+    IDX ro[kWsAhead][H];
+    bool rv[kWsAhead][H];
+    auto rows = [&](int blk, IDX (&o)[H], bool (&v)[H]) {
+#pragma unroll
+      for (int h = 0; h < H; ++h) {
+        const int r = blk * kRows + rl[h];
+        v[h] = blk < nblk && r < a.R;
+        o[h] = v[h] ? xr[r] : 0;
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < kWsAhead; ++d) rows(blockIdx.x + d * gridDim.x, ro[d], rv[d]);
+    for (int i0 = 0; blockIdx.x + i0 * gridDim.x < nblk; i0 += kWsAhead) {
+#pragma unroll
+      for (int d = 0; d < kWsAhead; ++d) {
+        const int i = i0 + d;
+        const int blk = blockIdx.x + i * gridDim.x;
+        if (blk >= nblk) break;
+        const int q = i % S;
+        if (i >= S) mbar_wait(&empty[q], ((i / S) - 1) & 1);
+        double* dst = xs + q * stage;
+        if (a.dbg & 2) {
+        } else if constexpr (ROWS_UNIT) {
+#pragma unroll 2
+          for (int k = warp; k < a.KP; k += kWsProd) {
+            const bool kin = k < a.K;
+            const IDX ko = xks[k];
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+              cp_async8(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), kin && rv[d][h]);
+          }
+        } else {
+          const int kk = lane & 7;
+          for (int k0 = 0; k0 < a.KP; k0 += 8) {
+            const int k = k0 + kk;
+            if (k < a.KP) {
+              const IDX ko = xks[k];
+#pragma unroll
+              for (int h = 0; h < H; ++h)
+                cp_async8(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), rv[d][h] && k < a.K);
+            }
+          }
+        }
+        mbar_cp_async_arrive(&full[q]);
+        rows(blockIdx.x + (i + kWsAhead) * gridDim.x, ro[d], rv[d]);
+      }
+    }
+    cp_async_wait_all();
+    return;
+  }
+  // ---- consumers: group grp takes the CTA's blocks i = grp, grp + CG, ..; warp cw of the group
+  // owns rows wr .. wr + 15 and columns wc .. wc + NP / 2 - 1 of each block
+  const int cw = (warp - kWsProd) & 7, grp = (warp - kWsProd) >> 3;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = 16 * (cw & 3), wc = (cw >> 2) * (a.NP / 2);
+  const int wp = wr + a.sw * (wr >> 4) + g;   // ring position of row wr + g
+  double yr[kWsMaxK4][NW];
+#pragma unroll
+  for (int k4 = 0; k4 < kWsMaxK4; ++k4)
+#pragma unroll
+    for (int j = 0; j < NW; ++j)
+      yr[k4][j] = 4 * k4 < a.KP ? ys[(4 * k4 + t) * yp + wc + 8 * j + g] : 0.0;
+  IDX cco[NW][2];
+#pragma unroll
+  for (int j = 0; j < NW; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) cco[j][e] = ccs[wc + 8 * j + 2 * t + e];
+  const bool full_cols = a.NC == a.NP;
+  // C's row offsets: fetched two of the group's blocks ahead (ring indexed by the unrolled d)
+  IDX cro[2][2];
+  auto crows = [&](int blk, IDX (&o)[2]) {
+    const int r0 = blk * kRows + wr + g;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) o[h] = (blk < nblk && r0 + 8 * h < a.R) ? cr[r0 + 8 * h] : 0;
+  };
+  crows(blockIdx.x + grp * gridDim.x, cro[0]);
+  crows(blockIdx.x + (grp + CG) * gridDim.x, cro[1]);
+  for (int i0 = grp; blockIdx.x + i0 * gridDim.x < nblk; i0 += 2 * CG) {
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const int i = i0 + d * CG;
+    const int blk = blockIdx.x + i * gridDim.x;
+    if (blk >= nblk) break;
+    const int q = i % S;
+    mbar_wait(&full[q], (i / S) & 1);
+    const double* xb = xs + q * stage;
+    double acc[NW][4];
+#pragma unroll
+    for (int j = 0; j < NW; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < kWsMaxK4; ++k4) {
+      if (4 * k4 < a.KP && !(a.dbg & 1)) {
+        const double a0 = xb[(4 * k4 + t) * xp + wp], a1 = xb[(4 * k4 + t) * xp + wp + 8];
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+          dmma16x8x4(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, yr[k4][j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[q]);
+    // epilogue from registers: rows wr + g (+8), columns wc + 8 j + 2 t (+1)
+    const int r0 = blk * kRows + wr + g;
+    if (a.dbg & 4) {
+    } else if (a.beta == 0.0 && r0 + 8 < a.R && full_cols) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) a.C[cro[d][h] + cco[j][e]] = a.alpha * acc[j][2 * h + e];
+    } else {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (r0 + 8 * h >= a.R) continue;
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (wc + 8 * j + 2 * t + e >= a.NC) continue;
+            double* p = a.C + (cro[d][h] + cco[j][e]);
+            double v = a.alpha * acc[j][2 * h + e];
+            if (a.beta != 0.0) v = fma(a.beta, *p, v);
+            *p = v;
+          }
+      }
+    }
+    crows(blockIdx.x + (i + 2 * CG) * gridDim.x, cro[d]);
+  }
+  }
+}
+
+template <typename IDX, bool ROWS_UNIT, int NW, int CG>
+static int launch_ws(const Args& a, int nsm, cudaStream_t s, int stages_env) {
+  const int fixed = a.KP * (a.NP + 4) * (int)sizeof(double) + (a.KP + a.NP) * (int)sizeof(IDX);
+  const int stage = a.KP * a.xp * (int)sizeof(double) + 2 * (int)sizeof(uint64_t);
+  // 6 stages: 5 blocks (80 KB at N = K = 32) in flight per SM; 8 measured slower on f2_00
+  // (130.6 vs 123.4 us), 4 about equal (125.2 us)
+  int S = (227 * 1024 - fixed - 64) / stage;
+  S = S > 6 ? 6 : S;
+  if (stages_env >= 2 && stages_env < S) S = stages_env;
+  if (S < 2) return 0;
+  const int smem = fixed + S * stage + 64;
+  auto kern = tc_skinny_ws_kernel<IDX, ROWS_UNIT, NW, CG>;
+  static std::atomic<int> attr[kMaxDevices];
+  if (!ensure_dyn_smem(kern, smem, attr)) return -1;
+  const int nblk = (a.R + kRows - 1) / kRows;
+  const int grid = nblk < nsm ? nblk : nsm;
+  kern<<<grid, 32 * (kWsProd + 8 * CG), smem, s>>>(a, S);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// Warp-specialised form for NP <= 32 and KP <= 32 (TC_SKINNY_WS = 0 turns it off; _CG = 1 | 2
+// consumer groups, _STAGES caps the ring; measurement overrides, read per call). Returns 0 when
+// it does not apply.
+template <typename IDX, bool ROWS_UNIT>
+static int launch_ws_dir(const Args& a, int nsm, cudaStream_t s) {
+  if (a.NP > 32 || a.KP > 4 * kWsMaxK4) return 0;
+  const char* e = getenv("TC_SKINNY_WS");
+  if (e && *e == '0') return 0;
+  const char* ecg = getenv("TC_SKINNY_WS_CG");
+  const char* est = getenv("TC_SKINNY_WS_STAGES");
+  const int cg = ecg && *ecg == '1' ? 1 : 2;
+  const int st = est ? atoi(est) : 0;
+  if (a.NP == 16)
+    return cg == 1 ? launch_ws<IDX, ROWS_UNIT, 1, 1>(a, nsm, s, st)
+                   : launch_ws<IDX, ROWS_UNIT, 1, 2>(a, nsm, s, st);
+  return cg == 1 ? launch_ws<IDX, ROWS_UNIT, 2, 1>(a, nsm, s, st)
+                 : launch_ws<IDX, ROWS_UNIT, 2, 2>(a, nsm, s, st);
+}
+
 template <typename IDX, bool ROWS_UNIT>
 static int launch_dir(const Args& a, int nsm, cudaStream_t s) {
+  const int w = launch_ws_dir<IDX, ROWS_UNIT>(a, nsm, s);
+  if (w != 0) return w;
   switch (a.NP / 16) {
     case 1: return launch_nw<IDX, ROWS_UNIT, 1>(a, nsm, s);
     case 2: return launch_nw<IDX, ROWS_UNIT, 2>(a, nsm, s);
@@ -308,6 +573,36 @@ int launch_skinny(const LaunchArgs& la, cudaStream_t stream, bool force) {
   a.alpha = la.alpha; a.beta = la.beta;
   a.bu = la.skinny_bu > 0 ? la.skinny_bu : 1;
   a.bv = la.skinny_bv > 0 ? la.skinny_bv : 1;
+  // Ring layout. A half-warp's 8-byte cp.async writes land in one shared-memory wavefront only
+  // if its 16 rows sit at distinct positions mod 16; the sub-divided row order puts lanes
+  // bv rows apart (bu = bv = 8: rows 0, 8, .., 56 -- 4-way conflicts, 13.5 M write wavefronts
+  // for 2.1 M of data on f2_00, profiles/r02/ncu/f2_00.summary.txt). Block row r is stored at
+  // r + sw (r / 16), sw the smallest skew that minimises the conflicts (the fragment reads
+  // take 16 consecutive rows, unaffected by a shift).
+  const char* sw_e = getenv("TC_SKINNY_SW");   // override, read per call (TC_SKINNY_SW = 0..4)
+  const int sw_env = sw_e && *sw_e ? atoi(sw_e) : -1;
+  a.sw = 0;
+  if (rows_unit) {
+    int best = 1 << 30;
+    for (int s = 0; s <= 4; ++s) {
+      int cost = 0;
+      for (int h0 = 0; h0 < kRows; h0 += 16) {   // the half-warps of the loader
+        int cnt[16] = {0}, mx = 0;
+        for (int e = h0; e < h0 + 16; ++e) {
+          const int bb = a.bu * a.bv;
+          const int r = (e % a.bu) * a.bv + (e / a.bu) % a.bv + (e / bb) * bb;
+          const int c = ++cnt[(r + s * (r >> 4)) & 15];
+          mx = c > mx ? c : mx;
+        }
+        cost += mx;
+      }
+      if (cost < best) { best = cost; a.sw = s; }
+    }
+  }
+  if (sw_env >= 0 && sw_env <= 4) a.sw = sw_env;
+  a.xp = a.sw ? kXPSkew : kXP;
+  const char* dbg_e = getenv("TC_SKINNY_DBG");
+  a.dbg = dbg_e ? atoi(dbg_e) : 0;
   if (la.idx64)
     return rows_unit ? launch_dir<long long, true>(a, la.num_sms, stream)
                      : launch_dir<long long, false>(a, la.num_sms, stream);

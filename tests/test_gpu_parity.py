@@ -776,6 +776,45 @@ def test_skinny_shapes(spec, lens, beta, skinny, monkeypatch):
     check(case, bitwise=True)
 
 
+@pytest.mark.parametrize("spec,lens", [
+    ("mn-mk-kn", {"m": 7001, "n": 32, "k": 32}),       # X = A along its rows, NP = KP = 32
+    ("mn-km-kn", {"m": 4099, "n": 17, "k": 9}),        # X = A along K, NP = 32, KP = 12
+    ("mn-mk-nk", {"m": 5, "n": 9000, "k": 31}),        # small M: X = B along its rows, NP = 16
+    ("mn-mk-kn", {"m": 3, "n": 5000, "k": 2}),         # small M: X = B along K
+    ("abcde-efbad-cf", {"a": 16, "b": 7, "c": 32, "d": 11, "e": 24, "f": 32}),   # sub-divided
+    ("mn-mk-kn", {"m": 300000, "n": 32, "k": 32}),     # many blocks per CTA (ring wraps)
+])
+@pytest.mark.parametrize("ws", ["0", "cg1", "cg2", "st2", "st3"])
+def test_skinny_warp_specialised(spec, lens, ws, monkeypatch):
+    """The skinny kernel's warp-specialised form (NP, KP <= 32): producer warps fill an S-deep
+    ring tracked by mbarriers, 1 or 2 consumer groups multiply and store; against the synchronous
+    form (ws = 0) and the oracle, bitwise on integer inputs, beta = 0 and beta != 0."""
+    monkeypatch.setenv("TC_SKINNY_WS", "0" if ws == "0" else "1")
+    monkeypatch.setenv("TC_SKINNY_WS_CG", "1" if ws == "cg1" else "2")
+    monkeypatch.setenv("TC_SKINNY_WS_STAGES", ws[2:] if ws.startswith("st") else "0")
+    lc, la, lb = spec.split("-")
+    for beta in (0.0, 0.5):
+        case = W.Case("skinny_ws_" + spec, lc, la, lb, lens, alpha=2.0, beta=beta, dist="int",
+                      c_init="dist" if beta else "nan", seed=41)
+        check(case, bitwise=True)
+
+
+@pytest.mark.parametrize("lens", [
+    {"a": 16, "b": 7, "c": 32, "d": 11, "e": 24, "f": 20},   # bu = bv = 8: skew 2
+    {"a": 12, "b": 9, "c": 17, "d": 13, "e": 8, "f": 33},    # bu = 8, bv = 4: skew 2
+    {"a": 8, "b": 10, "c": 40, "d": 9, "e": 12, "f": 8},     # bu = 4, bv = 8: skew 4
+])
+@pytest.mark.parametrize("sw", ["", "0", "1", "3"])
+def test_skinny_ring_skew(lens, sw, monkeypatch):
+    """The skinny kernel's skewed X ring (block row r at r + sw (r / 16), chosen on the host from
+    the sub-division (bu, bv); TC_SKINNY_SW forces one): every skew gives the oracle's result,
+    bitwise on integer inputs, with a ragged last block."""
+    monkeypatch.setenv("TC_SKINNY_SW", sw)
+    case = W.Case("skinny_skew", "abcde", "efbad", "cf", lens, alpha=2.0, beta=0.5,
+                  dist="int", c_init="dist", seed=37)
+    check(case, bitwise=True)
+
+
 # ---------------------------------------------------------------------------------------------
 # negative strides (accepted for A, B and C by the C ABI, reading R7) through the raw binding
 # ---------------------------------------------------------------------------------------------
