@@ -799,6 +799,25 @@ def test_skinny_warp_specialised(spec, lens, ws, monkeypatch):
         check(case, bitwise=True)
 
 
+@pytest.mark.parametrize("shift", [0, 1, 2])
+def test_skinny_offset_views(shift):
+    """The skinny kernel on an X viewed at an element offset (8-byte and 16-byte shifted bases),
+    ragged rows: bitwise equal to the oracle (integer inputs)."""
+    m, n, k = 5003, 32, 32
+    g = torch.Generator().manual_seed(7 + shift)
+    big = torch.randint(-8, 9, (m * k + 8,), generator=g).double()
+    A = big[shift:shift + m * k].view(k, m).t()          # column-major (m contiguous), offset
+    B = torch.randint(-8, 9, (k, n), generator=g).double()
+    C0 = torch.randint(-8, 9, (m, n), generator=g).double()
+    ref = C0.clone()
+    oracle.contract("mn-mk-kn", A, B, ref, 2.0, 0.5)
+    bigd = big.cuda()
+    Ad = bigd[shift:shift + m * k].view(k, m).t()
+    Cd = C0.cuda()
+    tc().contract("mn-mk-kn", Ad, B.cuda(), Cd, 2.0, 0.5)
+    assert torch.equal(Cd.cpu(), ref)
+
+
 @pytest.mark.parametrize("lens", [
     {"a": 16, "b": 7, "c": 32, "d": 11, "e": 24, "f": 20},   # bu = bv = 8: skew 2
     {"a": 12, "b": 9, "c": 17, "d": 13, "e": 8, "f": 33},    # bu = 8, bv = 4: skew 2
