@@ -143,6 +143,9 @@ __global__ void __launch_bounds__(kThreads, TC_RANKK_MINB) tc_rankk_kernel(Args 
 // i + kD are gathered through offsets that landed with block i's group), so no thread waits on a
 // dependent global load: version 1 stalled on its next block's two dependent loads (offsets,
 // then values) at every block. One __syncthreads per block remains. Stores as in version 1.
+#ifndef TC_RANKK_STNA
+#define TC_RANKK_STNA 1   // C stores skip L1 allocation (st.global.L1::no_allocate)
+#endif
 constexpr int kD = 3;   // units of B values in flight (offsets: 2 kD + 1; rings of kD + 1 and 2 kD + 2)
 
 template <typename T, typename IDX, int MAXK>
@@ -278,7 +281,11 @@ __global__ void __launch_bounds__(kThreads, MAXK <= 8 ? TC_RANKK_MINB : 4) tc_ra
             T* q = C + (rc[h] + cc);
             double v = p.alpha * acc[h][j];
             if (p.beta != 0.0) v = fma(p.beta, static_cast<double>(*q), v);
+#if TC_RANKK_STNA
+            st_na(q, static_cast<T>(v));
+#else
             *q = static_cast<T>(v);
+#endif
           }
         }
       }

@@ -296,13 +296,6 @@ constexpr int kWsProd = 4;
 constexpr int kWsMaxK4 = 8;   // KP <= 32
 constexpr int kWsAhead = 4;   // producer: row-offset lookahead (blocks)
 
-// C is written once and never re-read by the kernel: stores skip L1 allocation (stores-only
-// f2_00 66.1 -> 56.6 us, whole kernel 123.6 -> 120.8 us; .cs and an L2 evict-first policy measured
-// 122.6 / 126.0 us, profiles/r02/ab_skinny_ws.txt)
-__device__ __forceinline__ void st_c(double* p, double v) {
-  asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
-}
-
 template <typename IDX, bool ROWS_UNIT, int NW, int CG>
 __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kernel(Args a, int S) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -462,7 +455,9 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[q]);
-    // epilogue from registers: rows wr + g (+8), columns wc + 8 j + 2 t (+1)
+    // epilogue from registers: rows wr + g (+8), columns wc + 8 j + 2 t (+1). The streaming
+    // stores skip L1 allocation (stores-only f2_00 66.1 -> 56.6 us, whole kernel 123.6 -> 120.8;
+    // .cs / an L2 evict-first policy 122.6 / 126.0 us, profiles/r02/ab_skinny_ws.txt)
     const int r0 = blk * kRows + wr + g;
     if (a.dbg & 4) {
     } else if (a.beta == 0.0 && r0 + 8 < a.R && full_cols) {
@@ -471,7 +466,7 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
 #pragma unroll
         for (int j = 0; j < NW; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) st_c(a.C + (cro[d][h] + cco[j][e]), a.alpha * acc[j][2 * h + e]);
+          for (int e = 0; e < 2; ++e) st_na(a.C + (cro[d][h] + cco[j][e]), a.alpha * acc[j][2 * h + e]);
     } else {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
