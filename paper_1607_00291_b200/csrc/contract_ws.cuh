@@ -375,6 +375,14 @@ template <typename T, typename IDX, bool FIXED_VECS, int LD> struct GatherSel<T,
 //             north star for fp32): 16-byte shared loads along each layout's contiguous
 //             direction, 64 FFMA per 16 loaded values.
 // ------------------------------------------------------------------------------------------
+// Consumer warp w of the DMMA micro-kernel owns rows dmma_wm(w) .. + 63 and columns
+// dmma_wn(w) .. + 31 of the tile. Warps w and w + 4 share a sub-partition (SMSP, one DMMA unit):
+// they take opposite row halves and column quarters two apart, so on a ragged edge tile (rows
+// or columns cut, the cut-off warps skipping their empty MMAs, stage_edge) every SMSP keeps part
+// of the work -- the tile's time per K step is its busiest SMSP's (dmma_tile_weight).
+__host__ __device__ constexpr int dmma_wm(int w) { return ((w >> 2) & 1) * WM; }
+__host__ __device__ constexpr int dmma_wn(int w) { return ((w & 3) ^ (2 * ((w >> 2) & 1))) * WN; }
+
 template <typename T, bool A_VM, bool B_VK>
 struct MicroDmma {
   using Acc = double;
@@ -383,7 +391,7 @@ struct MicroDmma {
   Acc acc[8][8];      // row r = 2i+h: m = wm + 16i + g + 8h; col c = 2j+e: n = wn + 8j + 2t + e
   int wm, wn, g, t;
   __device__ __forceinline__ void setup(int warp, int lane) {
-    g = lane >> 2; t = lane & 3; wm = (warp & 1) * WM; wn = (warp >> 1) * WN;
+    g = lane >> 2; t = lane & 3; wm = dmma_wm(warp); wn = dmma_wn(warp);
   }
   __device__ __forceinline__ int row(int r) const { return wm + 16 * (r >> 1) + g + 8 * (r & 1); }
   __device__ __forceinline__ int col(int c) const { return wn + 8 * (c >> 1) + 2 * t + (c & 1); }
@@ -770,12 +778,12 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     if (beta != 0.0 && kb == 0 && ke - kb >= 4) {
       // pull the warp's 64 x 32 block of C into L2 while the K loop runs: lane l takes column
       // l and four 16-row runs (one 128-byte line each when C is contiguous along M)
-      const int n = n0 + (warp >> 1) * WN + lane;
+      const int n = n0 + mk.wn + lane;
       if (n < N) {
         const IDX c = cC[n];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int m = m0 + (warp & 1) * WM + 16 * q;
+          const int m = m0 + mk.wm + 16 * q;
           if (m < M) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + (rC[m] + c)));
         }
       }
@@ -823,7 +831,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
     if (split) {
       const int s_local = tile - sched.D;
       const long long g_first = (long long)s_local * sched.KT;
-      const int owner = (int)(((g_first + 1) * sched.P_sk + sched.I - 1) / sched.I) - 1;
+      const int owner = sk_owner(sched, g_first);
       piece = blockIdx.x - owner;
       flag = flags + s_local;
       if (piece > 0) {
@@ -1052,6 +1060,41 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
 }
 
 
+// Work weights of a ragged stream-K tail (Sched::weighted): a tile's time per K step is its
+// busiest SMSP's MMA count -- the two consumer warps of an SMSP (dmma_wm / dmma_wn), each doing
+// all 16 of its m16n8 blocks, or only the mi x nj that hold data when that is at most half
+// (the stage_edge rule) -- clamped to >= 1/4 of a full tile so no CTA's range is empty.
+// TC_SK_WEIGHTS=0 turns it off (read per call).
+inline void set_tile_weights(Sched& sc, int M, int N, int tiles_m, int tiles_n) {
+  const int n = sc.T - sc.D;
+  const char* e = getenv("TC_SK_WEIGHTS");
+  sc.weighted = 0;
+  // long K loops only: on short ones (cfg1, 12 us) the moved boundaries cost more than the
+  // balance gains (12.0 -> 14.5 us; f2_17 1034.6 -> 988.2 us, profiles/r02/ab_sk_weights.txt)
+  if (sc.P_sk == 0 || n > kMaxWeighted || sc.KT < 256 || (M % BM == 0 && N % BN == 0) ||
+      (e && *e == '0'))
+    return;
+  sc.cum[0] = 0;
+  bool any = false;
+  for (int i = 0; i < n; ++i) {
+    int tm, tn;
+    tile_coords<GROUP_M>(sc.D + i, tiles_m, tiles_n, &tm, &tn);
+    int smsp[4] = {0, 0, 0, 0};
+    for (int w = 0; w < NCW; ++w) {
+      int mi = (M - (tm * BM + dmma_wm(w)) + 15) / 16, nj = (N - (tn * BN + dmma_wn(w)) + 7) / 8;
+      mi = mi < 0 ? 0 : (mi > 4 ? 4 : mi);
+      nj = nj < 0 ? 0 : (nj > 4 ? 4 : nj);
+      smsp[w & 3] += mi * nj > 8 ? 16 : mi * nj;
+    }
+    int wt = 0;
+    for (int q = 0; q < 4; ++q) wt = smsp[q] > wt ? smsp[q] : wt;
+    wt = wt < 8 ? 8 : wt;
+    any = any || wt < 32;
+    sc.cum[i + 1] = sc.cum[i] + wt;
+  }
+  sc.weighted = any ? 1 : 0;
+}
+
 template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 int launch(const LaunchArgs& a, cudaStream_t stream) {
   constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
@@ -1073,6 +1116,7 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
     Sched dp = make_sched(tiles_m * tiles_n, KT, a.num_sms, false);
     sc = dp;
   }
+  if (!FFMA && TC_DMMA_EDGE) set_tile_weights(sc, a.M, a.N, tiles_m, tiles_n);
   int* flags = a.flags;
   sc.epoch = a.flag_epoch;
   const int grid = sc.D > 0 ? sc.P : sc.P_sk;

@@ -97,10 +97,11 @@ __device__ __forceinline__ void dmma16x8x4(double& d0, double& d1, double& d2, d
 // Tile rasterisation: GROUP_M consecutive M-tiles walk the N-tiles together so that CTAs
 // running at the same time share A and B panels in L2.
 template <int GROUP_M>
-__device__ __forceinline__ void tile_coords(int pid, int tiles_m, int tiles_n, int* tm, int* tn) {
+__host__ __device__ __forceinline__ void tile_coords(int pid, int tiles_m, int tiles_n, int* tm,
+                                                     int* tn) {
   const int group_size = GROUP_M * tiles_n;
   const int first_m = (pid / group_size) * GROUP_M;
-  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int gm = tiles_m - first_m < GROUP_M ? tiles_m - first_m : GROUP_M;
   *tm = first_m + (pid % group_size) % gm;
   *tn = (pid % group_size) / gm;
 }

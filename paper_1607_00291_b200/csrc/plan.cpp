@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 
 namespace tcb {
@@ -185,6 +186,13 @@ void span(int rank, const int64_t* lens, const int64_t* strides, int64_t* lo, in
 // addresses of padded rows, whose table entries are 0) is 16-byte aligned for a 16-byte
 // aligned base (V = 16 / element size), and the kernel moves each block with one 16-byte copy
 // without per-element checks.
+// TC_KBLOCK=flat: the one-level P sub-division only (measurement A/B of the second level).
+// Read per plan build (plans are cached by structure, so set it before the first call).
+static bool kblock_flat() {
+  const char* e = getenv("TC_KBLOCK");
+  return e && !strcmp(e, "flat");
+}
+
 static bool vec_blocks_all(const std::vector<int64_t>& vtab, const std::vector<int64_t>& other,
                            int64_t V) {
   if (vtab.empty() || other.empty() || vtab.size() % (size_t)V) return false;
@@ -317,8 +325,22 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
           return x;
         };
         std::vector<Dim> out = {part(du, bu, 1, "_lo"), part(dw, bw, 1, "_lo")};
-        if (du.len / bu > 1) out.push_back(part(du, du.len / bu, bu, "_hi"));
-        if (dw.len / bw > 1) out.push_back(part(dw, dw.len / bw, bw, "_hi"));
+        // Second level when both lengths allow it (bu = bw = 4, both lengths multiples of 16):
+        // [u_lo, w_lo, u_mid, w_mid, u_hi, w_hi], so every 16 consecutive K steps read whole
+        // 128-byte lines of both operands (u 0..15 x w 0..15) instead of 32-byte pieces whose
+        // line-mates come back 1/4 of the bundle later (fig:bench ab-cad-dcb: 3.6 GB of DRAM
+        // reads for 0.54 GB of operands, profiles/r02/ncu/f2_16_k2.summary.txt)
+        const bool mid = bu == 4 && bw == 4 && du.len % 16 == 0 && dw.len % 16 == 0 &&
+                         du.len > 16 && dw.len > 16 && !kblock_flat();
+        if (mid) {
+          out.push_back(part(du, 4, 4, "_mid"));
+          out.push_back(part(dw, 4, 4, "_mid"));
+          out.push_back(part(du, du.len / 16, 16, "_hi"));
+          out.push_back(part(dw, dw.len / 16, 16, "_hi"));
+        } else {
+          if (du.len / bu > 1) out.push_back(part(du, du.len / bu, bu, "_hi"));
+          if (dw.len / bw > 1) out.push_back(part(dw, dw.len / bw, bw, "_hi"));
+        }
         for (size_t i = 0; i < p->kb.P.size(); ++i)
           if ((int)i != u && (int)i != w) out.push_back(p->kb.P[i]);
         p->kb.P = out;

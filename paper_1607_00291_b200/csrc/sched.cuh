@@ -21,6 +21,8 @@ namespace sched {
 // add alpha*acc in a fixed order behind a per-tile flag. No partial-sum workspace, deterministic
 // results, and a piece only waits on lower-ranked CTAs' first work items (no deadlock).
 // ------------------------------------------------------------------------------------------
+constexpr int kMaxWeighted = 32;   // stream-K tail tiles that can carry work weights
+
 struct Sched {
   int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
   int P_sk;                 // CTAs in the stream-K tail (0: no tail)
@@ -35,7 +37,35 @@ struct Sched {
   // count in the low 8 bits: a value left behind by any earlier launch on the stream, finished
   // or aborted, never matches, so no per-launch reset is needed and none can be missed
   unsigned epoch;
+  // Work-weighted stream-K (weighted != 0; the DMMA kernel on ragged few-tile shapes): tail tile
+  // t costs w_t per K iteration (edge tiles skip empty MMAs and run faster), cum[t] = sum of
+  // w_t' for t' < t. CTA w takes the K iterations whose work lies in [w W / P_sk,
+  // (w + 1) W / P_sk), W = KT cum[T - D], instead of an equal number of iterations.
+  int weighted;
+  int cum[kMaxWeighted + 1];
 };
+
+// First stream-K iteration of CTA w (w = P_sk: the end).
+__host__ __device__ inline long long sk_bound(const Sched& s, int w) {
+  if (!s.weighted) return (long long)w * s.I / s.P_sk;
+  const int n = s.T - s.D;
+  const long long W = (long long)w * ((long long)s.KT * s.cum[n]) / s.P_sk;
+  int t = 0;
+  while (t + 1 < n && (long long)s.KT * s.cum[t + 1] <= W) ++t;
+  const long long wt = s.cum[t + 1] - s.cum[t], off = W - (long long)s.KT * s.cum[t];
+  return (long long)t * s.KT + (off + wt - 1) / wt;
+}
+// The CTA whose stream-K range holds iteration g.
+__host__ __device__ inline int sk_owner(const Sched& s, long long g) {
+  if (!s.weighted) return (int)(((g + 1) * s.P_sk + s.I - 1) / s.I) - 1;
+  int lo = 0, hi = s.P_sk;   // the largest w with sk_bound(w) <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (sk_bound(s, mid) <= g) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
 
 struct WorkIter {
   int dp_t, D, P, KT;
@@ -47,8 +77,8 @@ struct WorkIter {
     dp_t = w < s.P ? w : s.D;
     sk_t = -1; sk_lo = 0; g0 = g1 = 0;
     if (w < s.P_sk) {
-      g0 = (long long)w * s.I / s.P_sk;
-      g1 = (long long)(w + 1) * s.I / s.P_sk;
+      g0 = sk_bound(s, w);
+      g1 = sk_bound(s, w + 1);
       if (g1 > g0) { sk_t = (int)((g1 - 1) / KT); sk_lo = (int)(g0 / KT); }
     }
   }

@@ -210,3 +210,22 @@ def test_dimension_subdivision_of_the_bound_bundle():
     p = _check_traversal(case)
     cA, rB = p.traversal_scatter(1), p.traversal_scatter(2)
     assert cA[:4] == [0, 1, 2, 3] and rB[4:8] == [1, 1 + 4 * 7, 1 + 2 * 4 * 7, 1 + 3 * 4 * 7]
+
+
+def test_dimension_subdivision_of_the_bound_bundle_two_levels():
+    """f4 for P with both unit-stride lengths multiples of 16 (fig:bench ab-cad-dcb's class):
+    the K traversal is [k_lo 4, d_lo 4, k_mid 4, d_mid 4, k_hi, d_hi], so every 16 K steps of
+    16 read k 0..15 x d 0..15 -- whole 128-byte lines of both operands."""
+    lens = {"r": 3, "o": 2, "k": 32, "d": 48, "c": 5}
+    case = W.Case("sub_P2", "roc", "krdo", "dck", lens, dist="int", alpha=1.0, beta=0.5,
+                  c_init="dist", seed=6)
+    p = _check_traversal(case)
+    A, B, _ = W.make_tensors(case)
+    sk, sd = A.stride(0), A.stride(2)      # A = krdo
+    tk, td = B.stride(2), B.stride(0)      # B = dck
+    cA, rB = p.traversal_scatter(1), p.traversal_scatter(2)
+    for t in range(32 * 48):
+        k = t % 4 + 4 * ((t // 16) % 4) + 16 * ((t // 256) % 2)
+        d = (t // 4) % 4 + 4 * ((t // 64) % 4) + 16 * (t // 512)
+        assert cA[t] == k * sk + d * sd, t
+        assert rB[t] == k * tk + d * td, t

@@ -523,6 +523,21 @@ def test_stream_k_splits(mnk, beta):
     check(case, bitwise=True)
 
 
+@pytest.mark.parametrize("weights", ["1", "0"])
+@pytest.mark.parametrize("mnk", [(323, 323, 30000), (200, 300, 20000), (129, 1000, 9000),
+                                 (1000, 70, 5000), (300, 3000, 4000)])
+@pytest.mark.parametrize("beta", [0.0, 0.75])
+def test_stream_k_work_weights(mnk, beta, weights, monkeypatch):
+    """Ragged few-tile shapes (every tile in the stream-K tail, edge tiles skipping empty MMAs):
+    the work-weighted split (Sched::weighted, TC_SK_WEIGHTS) gives edge tiles' CTAs more K
+    iterations; results bitwise equal to the oracle's on integer inputs either way (the
+    ordered fix-up is unchanged, only the piece boundaries move)."""
+    monkeypatch.setenv("TC_SK_WEIGHTS", weights)
+    case = W.Case("skw", "mn", "mk", "kn", dict(zip("mnk", mnk)), alpha=0.5, beta=beta,
+                  dist="int", c_init="dist", seed=35)
+    check(case, bitwise=True)
+
+
 @pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.parametrize("mnk", [(100, 120, 20000), (1000, 1200, 700), (128 * 12, 128 * 13, 2000),
                                  (2366, 1012, 1935)])
