@@ -380,8 +380,13 @@ template <typename T, typename IDX, bool FIXED_VECS, int LD> struct GatherSel<T,
 // they take opposite row halves and column quarters two apart, so on a ragged edge tile (rows
 // or columns cut, the cut-off warps skipping their empty MMAs, stage_edge) every SMSP keeps part
 // of the work -- the tile's time per K step is its busiest SMSP's (dmma_tile_weight).
+#ifndef TC_DMMA_OLDMAP
 __host__ __device__ constexpr int dmma_wm(int w) { return ((w >> 2) & 1) * WM; }
 __host__ __device__ constexpr int dmma_wn(int w) { return ((w & 3) ^ (2 * ((w >> 2) & 1))) * WN; }
+#else   // measurement A/B: the previous map (warp w: rows (w & 1), columns w >> 1)
+__host__ __device__ constexpr int dmma_wm(int w) { return (w & 1) * WM; }
+__host__ __device__ constexpr int dmma_wn(int w) { return (w >> 1) * WN; }
+#endif
 
 template <typename T, bool A_VM, bool B_VK>
 struct MicroDmma {

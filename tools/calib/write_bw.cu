@@ -1,0 +1,63 @@
+// Write-only and read-only HBM streams on B200: 8-byte vs 16-byte per-lane accesses, plain vs
+// L1::no_allocate / .cs stores, grid = k x #SMs. The ceilings for the store-bound kernels
+// (rank-k's and the skinny kernel's C streams). Not part of the product path.
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
+  fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+template <int VEC, int HINT>
+__global__ void wr(double* __restrict__ p, long long n, double v) {
+  const long long stride = (long long)gridDim.x * blockDim.x * VEC;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC; i < n; i += stride) {
+    if constexpr (VEC == 1) {
+      if constexpr (HINT == 0) p[i] = v;
+      else if constexpr (HINT == 1) asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p + i), "d"(v) : "memory");
+      else asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p + i), "d"(v) : "memory");
+    } else {
+      if constexpr (HINT == 0) *reinterpret_cast<double2*>(p + i) = make_double2(v, v);
+      else if constexpr (HINT == 1) asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p + i), "d"(v), "d"(v) : "memory");
+      else asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + i), "d"(v), "d"(v) : "memory");
+    }
+  }
+}
+template <int VEC>
+__global__ void rd(const double* __restrict__ p, long long n, double* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x * VEC;
+  double s = 0;
+  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * VEC; i < n; i += stride) {
+    if constexpr (VEC == 1) s += p[i];
+    else { const double2 x = *reinterpret_cast<const double2*>(p + i); s += x.x + x.y; }
+  }
+  if (s == 1234.5) out[0] = s;
+}
+
+template <typename F>
+float best(F f) {
+  cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+  f(); CK(cudaDeviceSynchronize());
+  float m = 1e30f;
+  for (int r = 0; r < 10; ++r) {
+    CK(cudaEventRecord(a)); f(); CK(cudaEventRecord(b)); CK(cudaEventSynchronize(b));
+    float t; CK(cudaEventElapsedTime(&t, a, b)); m = t < m ? t : m;
+  }
+  return m;
+}
+
+int main() {
+  const long long n = 1ll << 28;   // 2 GiB of doubles (> L2)
+  double* p; CK(cudaMalloc(&p, n * 8)); double* out; CK(cudaMalloc(&out, 8));
+  CK(cudaMemset(p, 0, n * 8));
+  for (int k : {2, 4, 8}) {
+    const int grid = 148 * k, thr = 256;
+#define W(V, H) { float ms = best([&] { wr<V, H><<<grid, thr>>>(p, n, 1.0); }); \
+    printf("{\"kind\": \"write\", \"vec\": %d, \"hint\": %d, \"ctas_per_sm\": %d, \"gbs\": %.0f}\n", V, H, k, n * 8 / ms / 1e6); }
+    W(1, 0) W(1, 1) W(1, 2) W(2, 0) W(2, 1) W(2, 2)
+#define R(V) { float ms = best([&] { rd<V><<<grid, thr>>>(p, n, out); }); \
+    printf("{\"kind\": \"read\", \"vec\": %d, \"ctas_per_sm\": %d, \"gbs\": %.0f}\n", V, k, n * 8 / ms / 1e6); }
+    R(1) R(2)
+  }
+  return 0;
+}
