@@ -648,6 +648,18 @@ __device__ __forceinline__ void store_c(T* p, T v, bool keep) {
   else *p = v;
 }
 
+// Stream-K accumulation of an fp64 piece: C += v as a reduction at L2 (red.global.add.f64,
+// one IEEE add, the same result as the load-add-store it replaces; the fix-up order is still set
+// by the per-tile flags, and the piece's fence before publishing waits for the reductions). The
+// pieces of a split tile then no longer pay a load round trip per chunk of C between links of
+// the fix-up chain. TC_SK_RED=0 builds the load-add-store form (measurement A/B).
+#ifndef TC_SK_RED
+#define TC_SK_RED 1
+#endif
+__device__ __forceinline__ void red_add_c(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ void producers_sync() {
   asm volatile("bar.sync 2, %0;\n" ::"n"(NPT) : "memory");
 }
@@ -845,6 +857,10 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       }
     }
     const bool accumulate = split && piece > 0;
+    // (short K loops keep the load-add-store: with one or two K steps per piece the many
+    //  concurrent reductions cost more at L2 than they save; f1 k32 682 -> 717 us with red,
+    //  f2_07/08/10 -2..-6%; profiles/r02/ab_sk_red.txt)
+    const bool red = TC_SK_RED && std::is_same<T, double>::value && sched.KT >= 8;
     const bool keep_c = split && ke < sched.KT;   // a later piece reads this tile back
 
     if constexpr (FFMA) {
@@ -1004,7 +1020,19 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       cc[c] = wtab[WM + mk.col(c) - mk.wn];
     }
     const bool read_c = accumulate || beta != 0.0;
-    if (!read_c && m0 + BM <= M && n0 + BN <= N) {
+    if (red && accumulate) {
+      // stream-K accumulation at L2 (red_add_c): no reads, no round trips
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int m = m0 + mk.row(r);
+        const IDX rcr = wtab[mk.row(r) - mk.wm];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (m < M && nn[c] < N)
+            red_add_c(reinterpret_cast<double*>(C + (rcr + cc[c])),
+                      alpha * static_cast<double>(mk.value(r, c)));
+      }
+    } else if (!read_c && m0 + BM <= M && n0 + BN <= N) {
       // interior tile, C write-only: no bounds checks, no reads, all offsets up front (the
       // common case of small-K contractions, where the epilogue is most of the work)
       IDX rc[8];
@@ -1116,7 +1144,9 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   // up to 48 stream-K pieces per tile: few-tile, long-K shapes then keep every SM busy (this
   // kernel's fix-up links are cheap: 256^2 x 65536 0.39 -> 0.52, 128^2 x 262144 0.12 -> 0.27 of
   // DGEMM; profiles/r01/ab_max_pieces.txt)
-  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k, dp_pct, kMinSkIters, 48);
+  const char* msk = getenv("TC_WS_MINSK");   // measurement override of kMinSkIters (per call)
+  const int min_sk = msk && atoi(msk) > 0 ? atoi(msk) : kMinSkIters;
+  Sched sc = make_sched(tiles_m * tiles_n, KT, a.num_sms, a.stream_k, dp_pct, min_sk, 48);
   if (sc.P_sk > 0 && (sc.T - sc.D) > a.flags_cap) {   // cannot happen: S < 2 * num_sms
     Sched dp = make_sched(tiles_m * tiles_n, KT, a.num_sms, false);
     sc = dp;
