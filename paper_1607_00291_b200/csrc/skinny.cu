@@ -5,8 +5,9 @@
 // in shared memory for the whole kernel. The general 128 x 128 tile would spend most of its
 // DMMA work on padding and restart its pipeline every 2-5 K steps.
 //
-// Two forms. For NP, KP <= 32 (the HBM-bound class) a warp-specialised kernel (producer warps,
-// an mbarrier ring, consumer warps; tc_skinny_ws_kernel below). Otherwise:
+// Two forms. The default is warp-specialised (tc_skinny_ws_kernel below: producer warps, an
+// mbarrier ring, consumer warps; Y in registers for N, K <= 32). The synchronous form (kept for
+// TC_SKINNY_WS=0 and as the fallback when the ring does not fit):
 // Persistent CTAs (256 threads) each load Y once (gathered through its scatter
 // vectors), then walk 64-row blocks of X: a 2-3-deep ring of X blocks is gathered
 // with cp.async (coalesced element copies along X's unit-stride direction, written to the
@@ -293,10 +294,14 @@ static int launch_nw(const Args& a, int nsm, cudaStream_t s) {
 // multiply (Y held in registers for the CTA's lifetime), release the stage, and store C from
 // registers. Up to S - 1 blocks per SM are in flight while the consumers compute.
 constexpr int kWsProd = 4;
+// (larger resident operands, Y from shared memory, one consumer group: the N = K = 76 strings
+//  f2_02/04/06/12/13/14 1.06-1.18 -> 1.11-1.31 of DGEMM)
 constexpr int kWsMaxK4 = 8;   // KP <= 32
 constexpr int kWsAhead = 4;   // producer: row-offset lookahead (blocks)
 
-template <typename IDX, bool ROWS_UNIT, int NW, int CG>
+// YREG: Y's fragments live in registers (NP, KP <= 32); otherwise the consumers read them from
+// shared memory per block (block_mma), for the larger resident operands (K, N <= 80, 96).
+template <typename IDX, bool ROWS_UNIT, int NW, int CG, bool YREG>
 __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kernel(Args a, int S) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int yp = a.NP + 4, xp = a.xp, stage = a.KP * xp;
@@ -409,12 +414,14 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
   const int g = lane >> 2, t = lane & 3;
   const int wr = 16 * (cw & 3), wc = (cw >> 2) * (a.NP / 2);
   const int wp = wr + a.sw * (wr >> 4) + g;   // ring position of row wr + g
-  double yr[kWsMaxK4][NW];
+  double yr[YREG ? kWsMaxK4 : 1][NW];
+  if constexpr (YREG) {
 #pragma unroll
-  for (int k4 = 0; k4 < kWsMaxK4; ++k4)
+    for (int k4 = 0; k4 < kWsMaxK4; ++k4)
 #pragma unroll
-    for (int j = 0; j < NW; ++j)
-      yr[k4][j] = 4 * k4 < a.KP ? ys[(4 * k4 + t) * yp + wc + 8 * j + g] : 0.0;
+      for (int j = 0; j < NW; ++j)
+        yr[k4][j] = 4 * k4 < a.KP ? ys[(4 * k4 + t) * yp + wc + 8 * j + g] : 0.0;
+  }
   IDX cco[NW][2];
 #pragma unroll
   for (int j = 0; j < NW; ++j)
@@ -440,18 +447,22 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
     mbar_wait(&full[q], (i / S) & 1);
     const double* xb = xs + q * stage;
     double acc[NW][4];
+    if constexpr (YREG) {
 #pragma unroll
-    for (int j = 0; j < NW; ++j)
+      for (int j = 0; j < NW; ++j)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
+        for (int e = 0; e < 4; ++e) acc[j][e] = 0.0;
 #pragma unroll
-    for (int k4 = 0; k4 < kWsMaxK4; ++k4) {
-      if (4 * k4 < a.KP && !(a.dbg & 1)) {
-        const double a0 = xb[(4 * k4 + t) * xp + wp], a1 = xb[(4 * k4 + t) * xp + wp + 8];
+      for (int k4 = 0; k4 < kWsMaxK4; ++k4) {
+        if (4 * k4 < a.KP && !(a.dbg & 1)) {
+          const double a0 = xb[(4 * k4 + t) * xp + wp], a1 = xb[(4 * k4 + t) * xp + wp + 8];
 #pragma unroll
-        for (int j = 0; j < NW; ++j)
-          dmma16x8x4(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, yr[k4][j]);
+          for (int j = 0; j < NW; ++j)
+            dmma16x8x4(acc[j][0], acc[j][1], acc[j][2], acc[j][3], a0, a1, yr[k4][j]);
+        }
       }
+    } else {
+      block_mma<IDX, NW>(xb, xp, ys, yp, a.KP, wp - g, wc, g, t, acc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[q]);
@@ -488,18 +499,21 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
   }
 }
 
-template <typename IDX, bool ROWS_UNIT, int NW, int CG>
+template <typename IDX, bool ROWS_UNIT, int NW, int CG, bool YREG = true>
 static int launch_ws(const Args& a, int nsm, cudaStream_t s, int stages_env) {
   const int fixed = a.KP * (a.NP + 4) * (int)sizeof(double) + (a.KP + a.NP) * (int)sizeof(IDX);
   const int stage = a.KP * a.xp * (int)sizeof(double) + 2 * (int)sizeof(uint64_t);
-  // 6 stages: 5 blocks (80 KB at N = K = 32) in flight per SM; 8 measured slower on f2_00
-  // (130.6 vs 123.4 us), 4 about equal (125.2 us)
+  // Y in registers (N, K <= 32): 6 stages, 5 blocks (80 KB) in flight per SM; 8 measured
+  // slower on f2_00 (130.6 vs 123.4 us), 4 about equal (125.2), 3 139.6 us. Y in shared memory
+  // (N, K up to 96, 80): 2 stages -- more in flight measured slower on every such string
+  // (f2_02 237.6 / 240.4 / 266.1 us at 2 / 3 / 4 stages; profiles/r02/ab_skinny_ws.txt)
   int S = (227 * 1024 - fixed - 64) / stage;
-  S = S > 6 ? 6 : S;
+  const int cap = YREG ? 6 : 2;
+  S = S > cap ? cap : S;
   if (stages_env >= 2 && stages_env < S) S = stages_env;
   if (S < 2) return 0;
   const int smem = fixed + S * stage + 64;
-  auto kern = tc_skinny_ws_kernel<IDX, ROWS_UNIT, NW, CG>;
+  auto kern = tc_skinny_ws_kernel<IDX, ROWS_UNIT, NW, CG, YREG>;
   static std::atomic<int> attr[kMaxDevices];
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int nblk = (a.R + kRows - 1) / kRows;
@@ -508,18 +522,30 @@ static int launch_ws(const Args& a, int nsm, cudaStream_t s, int stages_env) {
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-// Warp-specialised form for NP <= 32 and KP <= 32 (TC_SKINNY_WS = 0 turns it off; _CG = 1 | 2
-// consumer groups, _STAGES caps the ring; measurement overrides, read per call). Returns 0 when
-// it does not apply.
+// Warp-specialised form (TC_SKINNY_WS = 0 turns it off, _WS_BIG = 0 for the larger resident
+// operands only; _CG = 1 | 2 consumer groups (Y in registers), _STAGES caps the ring;
+// measurement overrides, read per call). Returns 0 when it does not apply.
 template <typename IDX, bool ROWS_UNIT>
 static int launch_ws_dir(const Args& a, int nsm, cudaStream_t s) {
-  if (a.NP > 32 || a.KP > 4 * kWsMaxK4) return 0;
   const char* e = getenv("TC_SKINNY_WS");
   if (e && *e == '0') return 0;
   const char* ecg = getenv("TC_SKINNY_WS_CG");
   const char* est = getenv("TC_SKINNY_WS_STAGES");
   const int cg = ecg && *ecg == '1' ? 1 : 2;
   const int st = est ? atoi(est) : 0;
+  if (a.NP > 32 || a.KP > 4 * kWsMaxK4) {
+    // larger resident operand: Y's fragments from shared memory, one consumer group
+    const char* eb = getenv("TC_SKINNY_WS_BIG");
+    if (eb && *eb == '0') return 0;
+    switch (a.NP / 16) {
+      case 1: return launch_ws<IDX, ROWS_UNIT, 1, 1, false>(a, nsm, s, st);
+      case 2: return launch_ws<IDX, ROWS_UNIT, 2, 1, false>(a, nsm, s, st);
+      case 3: return launch_ws<IDX, ROWS_UNIT, 3, 1, false>(a, nsm, s, st);
+      case 4: return launch_ws<IDX, ROWS_UNIT, 4, 1, false>(a, nsm, s, st);
+      case 5: return launch_ws<IDX, ROWS_UNIT, 5, 1, false>(a, nsm, s, st);
+      default: return launch_ws<IDX, ROWS_UNIT, 6, 1, false>(a, nsm, s, st);
+    }
+  }
   if (a.NP == 16)
     return cg == 1 ? launch_ws<IDX, ROWS_UNIT, 1, 1>(a, nsm, s, st)
                    : launch_ws<IDX, ROWS_UNIT, 1, 2>(a, nsm, s, st);

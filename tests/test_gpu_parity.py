@@ -798,15 +798,20 @@ def test_skinny_shapes(spec, lens, beta, skinny, monkeypatch):
     ("mn-mk-kn", {"m": 3, "n": 5000, "k": 2}),         # small M: X = B along K
     ("abcde-efbad-cf", {"a": 16, "b": 7, "c": 32, "d": 11, "e": 24, "f": 32}),   # sub-divided
     ("mn-mk-kn", {"m": 300000, "n": 32, "k": 32}),     # many blocks per CTA (ring wraps)
+    ("mn-mk-kn", {"m": 70001, "n": 76, "k": 76}),      # Y fragments from shared memory, NP = 80
+    ("mn-km-kn", {"m": 4099, "n": 96, "k": 80}),       # largest resident operand, X along K
+    ("abcd-dbea-ec", {"a": 16, "b": 12, "c": 40, "d": 24, "e": 36}),   # fig:bench 2, sub-divided
 ])
-@pytest.mark.parametrize("ws", ["0", "cg1", "cg2", "st2", "st3"])
+@pytest.mark.parametrize("ws", ["0", "cg1", "cg2", "st2", "st3", "big0"])
 def test_skinny_warp_specialised(spec, lens, ws, monkeypatch):
-    """The skinny kernel's warp-specialised form (NP, KP <= 32): producer warps fill an S-deep
-    ring tracked by mbarriers, 1 or 2 consumer groups multiply and store; against the synchronous
-    form (ws = 0) and the oracle, bitwise on integer inputs, beta = 0 and beta != 0."""
+    """The skinny kernel's warp-specialised form: producer warps fill an S-deep ring tracked by
+    mbarriers, 1 or 2 consumer groups multiply (Y in registers for NP, KP <= 32, else from
+    shared memory) and store; against the synchronous form (ws = 0, big0 for the larger resident
+    operands) and the oracle, bitwise on integer inputs, beta = 0 and beta != 0."""
     monkeypatch.setenv("TC_SKINNY_WS", "0" if ws == "0" else "1")
     monkeypatch.setenv("TC_SKINNY_WS_CG", "1" if ws == "cg1" else "2")
     monkeypatch.setenv("TC_SKINNY_WS_STAGES", ws[2:] if ws.startswith("st") else "0")
+    monkeypatch.setenv("TC_SKINNY_WS_BIG", "0" if ws == "big0" else "1")
     lc, la, lb = spec.split("-")
     for beta in (0.0, 0.5):
         case = W.Case("skinny_ws_" + spec, lc, la, lb, lens, alpha=2.0, beta=beta, dist="int",
