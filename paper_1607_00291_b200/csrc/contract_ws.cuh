@@ -660,6 +660,30 @@ __device__ __forceinline__ void red_add_c(double* p, double v) {
   asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
 }
 
+// ---- cluster split-K (Sched::csplit) ----------------------------------------------------------
+// Each CTA of a cluster leaves its fp64 partial tile in its own (now idle) ring memory as
+// part[col][row] (pitch kPP), the cluster synchronises, and CTA r sums rows [r 128 / S,
+// (r + 1) 128 / S) of all S partials, read through distributed shared memory in rank order,
+// then writes alpha * sum + beta * C. A second cluster barrier keeps every CTA's shared memory
+// alive until all reads are done.
+constexpr int kPP = BM + 4;   // partial tile pitch (doubles), [col][row]
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ double ld_dsmem(uint32_t local, uint32_t rank) {
+  uint32_t remote;
+  double v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void producers_sync() {
   asm volatile("bar.sync 2, %0;\n" ::"n"(NPT) : "memory");
 }
@@ -696,6 +720,14 @@ constexpr int ring_stages() {
   return st;
 }
 
+// cluster split-K needs fp64 DMMA and a ring at least as large as the partial tile
+template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA>
+constexpr bool csk_fits() {
+  return !FFMA && std::is_same<T, double>::value &&
+         ring_stages<T, A_VM, B_VK, IDX, FFMA>() * (ALay<T, A_VM>::STAGE + BLay<T, B_VK>::STAGE) *
+                 (int)sizeof(T) >= BN * kPP * (int)sizeof(double);
+}
+
 template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 __global__ void __launch_bounds__(NTHREADS, 1)
 tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
@@ -708,6 +740,7 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
   using AL = ALay<T, A_VM>;
   using BL = BLay<T, B_VK>;
   constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
+  constexpr bool kCsk = csk_fits<T, A_VM, B_VK, IDX, FFMA>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);
   T* Bs = As + STAGES * AL::STAGE;
@@ -774,6 +807,10 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       }
     }
     cp_async_wait_all();
+    if (sched.csplit) {   // the consumers' two cluster barriers (partials written, sums read)
+      cluster_sync_all();
+      cluster_sync_all();
+    }
     return;
   }
 
@@ -840,6 +877,41 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
       if (lane == 0) mbar_arrive(&empty[s]);
     }
 
+    if constexpr (kCsk) {
+      if (sched.csplit) {
+        consumers_sync();   // every consumer warp is done with the ring: it holds the partial
+        double* part = reinterpret_cast<double*>(smem_raw);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            part[mk.col(c) * kPP + mk.row(r)] = static_cast<double>(mk.value(r, c));
+        cluster_sync_all();
+        const int S = sched.csplit, RS = BM / S;
+        const uint32_t rank = cluster_rank();
+        for (int e = threadIdx.x; e < RS * BN; e += NCW * 32) {
+          const int row = (int)rank * RS + e % RS, col = e / RS;
+          const uint32_t loc = smem_u32(part + col * kPP + row);
+          double v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = q < S ? ld_dsmem(loc, (uint32_t)q) : 0.0;
+          double sum = 0.0;
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (q < S) sum += v[q];
+          const int m = m0 + row, n = n0 + col;
+          if (m < M && n < N) {
+            T* q = C + (rC[m] + cC[n]);
+            double out = alpha * sum;
+            if (beta != 0.0) out = fma(beta, static_cast<double>(*q), out);
+            store_c(q, static_cast<T>(out), false);
+          }
+        }
+        cp_async_wait_all();
+        cluster_sync_all();
+        continue;
+      }
+    }
     // stream-K piece order: piece 0 (kb == 0) writes alpha*acc + beta*C; piece j >= 1 waits
     // for flag == j and adds alpha*acc; a piece that is not the last publishes flag = j + 1.
     const bool split = sk && !(kb == 0 && ke == sched.KT);
@@ -1128,6 +1200,62 @@ inline void set_tile_weights(Sched& sc, int M, int N, int tiles_m, int tiles_n) 
   sc.weighted = any ? 1 : 0;
 }
 
+// Cluster split-K instead of the stream-K schedule (Sched::csplit) where the stream-K split
+// would chain >= 4 pieces per tile (every tile in the tail): the largest S in {8, 4} (16,
+// non-portable, with TC_CSK_MAX=16) whose T clusters are co-resident in one wave (clusters must
+// sit inside a GPC: at 227 KB per CTA only 15 clusters of 8 and 33 of 4 fit on a B200, so 16
+// tiles in clusters of 8 take two waves) and whose T S CTAs cover >= 80% of the SMs stream-K
+// would use, with >= 2 K steps per CTA. TC_CSK=0 turns it off (read per call).
+template <typename K>
+inline int max_active_clusters(K kern, int S, int smem) {
+  static std::atomic<int> cache[kMaxDevices][5];   // S = 1 << (i + 0): 1, 2, 4, 8, 16
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+  const int i = S == 16 ? 4 : S == 8 ? 3 : S == 4 ? 2 : S == 2 ? 1 : 0;
+  int v = cache[dev][i].load(std::memory_order_relaxed);
+  if (v > 0) return v - 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)S);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (S > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                   cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  cache[dev][i].store(n + 1, std::memory_order_relaxed);
+  return n;
+}
+
+template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA, typename Kern>
+inline int csk_split(const Sched& sc, int nsm, bool allow, Kern kern, int smem) {
+  if constexpr (!csk_fits<T, A_VM, B_VK, IDX, FFMA>()) {
+    return 0;
+  } else {
+    const char* e = getenv("TC_CSK");
+    if (!allow || (e && *e == '0') || sc.D != 0 || sc.P_sk < 4 * sc.T) return 0;
+    const char* em = getenv("TC_CSK_MAX");
+    const int smax = em && atoi(em) == 16 ? 16 : 8;
+    for (int S = smax; S >= 4; S /= 2)
+      if (sc.T * S <= nsm && sc.KT >= 2 * S && 5 * sc.T * S >= 4 * sc.P_sk &&
+          sc.T <= max_active_clusters(kern, S, smem))
+        return S;
+    return 0;
+  }
+}
+
 template <typename T, typename IDX, bool A_VM, bool B_VK, int A_MODE, int B_MODE, bool FFMA>
 int launch(const LaunchArgs& a, cudaStream_t stream) {
   constexpr int STAGES = ring_stages<T, A_VM, B_VK, IDX, FFMA>();
@@ -1154,7 +1282,38 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   if (!FFMA && TC_DMMA_EDGE) set_tile_weights(sc, a.M, a.N, tiles_m, tiles_n);
   int* flags = a.flags;
   sc.epoch = a.flag_epoch;
-  const int grid = sc.D > 0 ? sc.P : sc.P_sk;
+  int grid = sc.D > 0 ? sc.P : sc.P_sk;
+  const int S = csk_split<T, A_VM, B_VK, IDX, FFMA>(sc, a.num_sms, a.stream_k, kern, smem);
+  if (S > 0) {
+    Sched cs = make_sched(sc.T, KT, a.num_sms, false);
+    cs.csplit = S;
+    cs.epoch = a.flag_epoch;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(sc.T * S));
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (getenv("TC_CSK_DEBUG")) {
+      int ncl = -1;
+      cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+      fprintf(stderr, "csk: T %d S %d KT %d max active clusters %d\n", sc.T, S, KT, ncl);
+    }
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(a.A), static_cast<const T*>(a.B),
+                           static_cast<T*>(a.C), static_cast<const IDX*>(a.rA),
+                           static_cast<const IDX*>(a.cA), static_cast<const IDX*>(a.rB),
+                           static_cast<const IDX*>(a.cB), static_cast<const IDX*>(a.rC),
+                           static_cast<const IDX*>(a.cC), a.vA, a.vB, a.M, a.N, a.K, tiles_m,
+                           tiles_n, a.alpha, a.beta, cs, flags, a.c_lanes_n) != cudaSuccess)
+      return -1;
+    return 1;
+  }
   // wave alignment only pays when a tile's K panels are long enough for L2 sharing to matter;
   // with short K loops the per-wave wait is pure overhead (f1 k5: 15% of samples at the barrier)
   sc.wave_sync = a.wave_sync && a.wave_base != nullptr && sc.D >= 2 * sc.P && KT >= 64;

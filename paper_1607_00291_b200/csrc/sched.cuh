@@ -43,6 +43,11 @@ struct Sched {
   // (w + 1) W / P_sk), W = KT cum[T - D], instead of an equal number of iterations.
   int weighted;
   int cum[kMaxWeighted + 1];
+  // Cluster split-K (csplit = S > 0; the DMMA kernel on few-tile problems): the grid is T x S
+  // CTAs in clusters of S, cluster t computes tile t, its CTA of rank r the K iterations
+  // [r KT / S, (r + 1) KT / S); the S partial tiles are summed through distributed shared
+  // memory in rank order (no flags, no fix-up chain).
+  int csplit;
 };
 
 // First stream-K iteration of CTA w (w = P_sk: the end).
@@ -70,10 +75,20 @@ __host__ __device__ inline int sk_owner(const Sched& s, long long g) {
 struct WorkIter {
   int dp_t, D, P, KT;
   int sk_t, sk_lo;          // current / lowest stream-K tile (relative to D), descending
+  int cs_kb, cs_ke;         // K range of a data-parallel item (cluster split-K: a share)
   long long g0, g1;         // this CTA's stream-K iteration range
 
   __device__ __forceinline__ void init(const Sched& s, int w) {
     D = s.D; P = s.P; KT = s.KT;
+    if (s.csplit) {   // one item: tile w / S, the rank's share of K (as a data-parallel item)
+      const int r = w % s.csplit;
+      dp_t = w / s.csplit; D = dp_t + 1; P = 1;
+      cs_kb = (int)((long long)r * KT / s.csplit);
+      cs_ke = (int)((long long)(r + 1) * KT / s.csplit);
+      sk_t = -1; sk_lo = 0; g0 = g1 = 0;
+      return;
+    }
+    cs_kb = 0; cs_ke = KT;
     dp_t = w < s.P ? w : s.D;
     sk_t = -1; sk_lo = 0; g0 = g1 = 0;
     if (w < s.P_sk) {
@@ -84,7 +99,7 @@ struct WorkIter {
   }
   // next work item: tile index, K-iteration range [kb, ke), stream-K piece flag
   __device__ __forceinline__ bool next(int& tile, int& kb, int& ke, bool& sk) {
-    if (dp_t < D) { tile = dp_t; dp_t += P; kb = 0; ke = KT; sk = false; return true; }
+    if (dp_t < D) { tile = dp_t; dp_t += P; kb = cs_kb; ke = cs_ke; sk = false; return true; }
     if (sk_t >= sk_lo) {
       const long long base = (long long)sk_t * KT;
       kb = (int)(g0 > base ? g0 - base : 0);

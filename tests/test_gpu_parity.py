@@ -538,6 +538,25 @@ def test_stream_k_work_weights(mnk, beta, weights, monkeypatch):
     check(case, bitwise=True)
 
 
+@pytest.mark.parametrize("csk", ["0", "8", "16"])
+@pytest.mark.parametrize("mnk", [(512, 512, 512), (323, 323, 3000), (200, 700, 1000),
+                                 (1024, 1024, 600), (130, 129, 70)])
+@pytest.mark.parametrize("beta", [0.0, 0.75])
+def test_cluster_split_k(mnk, beta, csk, monkeypatch):
+    """Few-tile fp64 shapes through cluster split-K (Sched::csplit: S CTAs of a cluster share a
+    tile's K loop, partials summed in rank order through distributed shared memory; S up to 8,
+    or 16 non-portable with TC_CSK_MAX=16) and through the stream-K fix-up chain (TC_CSK=0):
+    bitwise equal to the oracle on integer inputs, ragged edges, beta != 0, both C layouts."""
+    monkeypatch.setenv("TC_CSK", "0" if csk == "0" else "1")
+    monkeypatch.setenv("TC_CSK_MAX", "16" if csk == "16" else "8")
+    m, n, k = mnk
+    for spec in ("mn-mk-kn", "nm-km-nk"):
+        lc, la, lb = spec.split("-")
+        case = W.Case("csk_" + spec, lc, la, lb, {"m": m, "n": n, "k": k}, alpha=0.5, beta=beta,
+                      dist="int", c_init="dist", seed=57)
+        check(case, bitwise=True)
+
+
 @pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.parametrize("mnk", [(100, 120, 20000), (1000, 1200, 700), (128 * 12, 128 * 13, 2000),
                                  (2366, 1012, 1935)])
