@@ -1,4 +1,4 @@
-// Write-only and read-only HBM streams on B200: 8-byte vs 16-byte per-lane accesses, plain vs
+// Write-only and read-only HBM streams on B200: 8-, 16- and 32-byte per-lane accesses, plain vs
 // L1::no_allocate / .cs stores, grid = k x #SMs. The ceilings for the store-bound kernels
 // (rank-k's and the skinny kernel's C streams). Not part of the product path.
 #include <cstdio>
@@ -16,11 +16,27 @@ __global__ void wr(double* __restrict__ p, long long n, double v) {
       if constexpr (HINT == 0) p[i] = v;
       else if constexpr (HINT == 1) asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p + i), "d"(v) : "memory");
       else asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p + i), "d"(v) : "memory");
+    } else if constexpr (VEC == 4) {
+      if constexpr (HINT == 0) asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "d"(v), "d"(v), "d"(v), "d"(v) : "memory");
+      else if constexpr (HINT == 1) asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "d"(v), "d"(v), "d"(v), "d"(v) : "memory");
+      else asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "d"(v), "d"(v), "d"(v), "d"(v) : "memory");
     } else {
       if constexpr (HINT == 0) *reinterpret_cast<double2*>(p + i) = make_double2(v, v);
       else if constexpr (HINT == 1) asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1, %2};" ::"l"(p + i), "d"(v), "d"(v) : "memory");
       else asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p + i), "d"(v), "d"(v) : "memory");
     }
+  }
+}
+// one-shot grid (no grid-stride loop): CTA b writes its own contiguous chunk of CH doubles and
+// exits, the way torch's elementwise kernels (fill_ 7.4 TB/s) walk memory
+template <int VEC, int CH, int THR>
+__global__ void __launch_bounds__(THR) wr_chunk(double* __restrict__ p, double v) {
+  double* q = p + (long long)blockIdx.x * CH;
+#pragma unroll 4
+  for (int i = threadIdx.x * VEC; i < CH; i += THR * VEC) {
+    if constexpr (VEC == 1) q[i] = v;
+    else if constexpr (VEC == 2) *reinterpret_cast<double2*>(q + i) = make_double2(v, v);
+    else asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(q + i), "d"(v), "d"(v), "d"(v), "d"(v) : "memory");
   }
 }
 template <int VEC>
@@ -54,10 +70,14 @@ int main() {
     const int grid = 148 * k, thr = 256;
 #define W(V, H) { float ms = best([&] { wr<V, H><<<grid, thr>>>(p, n, 1.0); }); \
     printf("{\"kind\": \"write\", \"vec\": %d, \"hint\": %d, \"ctas_per_sm\": %d, \"gbs\": %.0f}\n", V, H, k, n * 8 / ms / 1e6); }
-    W(1, 0) W(1, 1) W(1, 2) W(2, 0) W(2, 1) W(2, 2)
+    W(1, 0) W(1, 1) W(1, 2) W(2, 0) W(2, 1) W(2, 2) W(4, 0) W(4, 1) W(4, 2)
 #define R(V) { float ms = best([&] { rd<V><<<grid, thr>>>(p, n, out); }); \
     printf("{\"kind\": \"read\", \"vec\": %d, \"ctas_per_sm\": %d, \"gbs\": %.0f}\n", V, k, n * 8 / ms / 1e6); }
     R(1) R(2)
   }
+#define WC(V, CH, THR) { float ms = best([&] { wr_chunk<V, CH, THR><<<(unsigned)(n / CH), THR>>>(p, 1.0); }); \
+    printf("{\"kind\": \"write_chunk\", \"vec\": %d, \"chunk_doubles\": %d, \"threads\": %d, \"gbs\": %.0f}\n", V, CH, THR, n * 8 / ms / 1e6); }
+  WC(1, 512, 128) WC(2, 1024, 128) WC(4, 2048, 128) WC(2, 4096, 256) WC(4, 8192, 256) WC(2, 16384, 256)
+  WC(1, 2048, 256) WC(2, 2048, 256) WC(4, 4096, 128)
   return 0;
 }
