@@ -40,6 +40,14 @@ struct LaunchArgs {
   bool c_lanes_n;
   int skinny_bu, skinny_bv;
   int tiny_mn_log2, tiny_mnk_log2;   // tiny.cu applies up to 2^mn elements of C, 2^mnk FMAs   // skinny kernel: X rows come in bv runs of bu (plan.cpp)        // FFMA epilogue: C's unit stride runs along N (lanes take columns)  // fp32 with A and B K-contiguous: transposing gather of A (mode 3)   // the plan prefers the element gather when not all vectors qualify
+  // fp32, B gathered along N without aligned vectors: shifted 16-byte N vectors (umma_f32.cu
+  // gather mode 12) through the per-tile-block run tables of tc_api.cpp nshift_tables:
+  // bsh_p[tn][slot] = (block offset, run length and shift) pairs (int2), bsh_c[tn][n] = staging
+  // word; b_shift: 0 = not available (no tables, B not 16-byte aligned, TC_UMMA_SHIFT=0),
+  // 1 = available (the kernel decides), 2 = forced where available (TC_UMMA_SHIFT=2)
+  const int* bsh_p;
+  const int* bsh_c;
+  int b_shift;
   int num_sms;        // persistent grid size (SMs of the current device)
   bool stream_k;      // split the final partial wave by K iterations
   bool f32_dmma;      // fp32 through the DMMA micro-kernel (fp64 accumulation) instead of FFMA

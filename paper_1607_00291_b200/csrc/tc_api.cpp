@@ -1,6 +1,7 @@
 // C ABI (include/tc.h): validation, plan cache, device tables, host (end-to-end) path.
 #include <algorithm>
 #include <atomic>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -47,6 +48,8 @@ struct DeviceTables {
   uint8_t* vA = nullptr;
   uint8_t* vB = nullptr;
   uint8_t* vZ = nullptr;   // all-zero flags as long as vA and vB (TC_FORCE_PATH=scatter)
+  int* bsh_p = nullptr;    // shifted N-vector tables of B (fp32 gather mode 12), or null
+  int* bsh_c = nullptr;
   ~DeviceTables() {
     int cur = -1;
     cudaGetDevice(&cur);
@@ -55,6 +58,8 @@ struct DeviceTables {
     cudaFree(vA);
     cudaFree(vB);
     cudaFree(vZ);
+    cudaFree(bsh_p);
+    cudaFree(bsh_c);
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
@@ -142,6 +147,48 @@ static cudaError_t upload_bytes(const std::vector<uint8_t>& v, uint8_t** out) {
   return cudaMemcpy(*out, v.data(), v.size(), cudaMemcpyHostToDevice);
 }
 
+// Shifted N-vector tables of an N-contiguous fp32 B (umma_f32.cu gather mode 12; the
+// block-scatter decision of P:644-683 taken per run instead of per aligned vector). Per tile
+// block of 128 columns, cscat_B splits into runs of consecutive addresses. Run j (first column
+// s, length L, offset b = cscat_B[s], c = b mod 4) owns ceil((L + 6) / 4) 16-byte slots of the
+// [k][n] staging, filled for K index k with the aligned blocks starting at
+// (b - c) + (rscat_B[k] - rscat_B[k] mod 4) + 4 i, so column n of k lands at staging word
+// 4 * first slot + c + (n - s) + rscat_B[k] mod 4: a per-column base plus a per-k shift.
+// prod[tn][slot] = (b - c + 4 i, L << 12 | (c - 4 i + 2048)) (block i of the run; unused slots
+// (0, 1948): never copied); conv[tn][n] = 4 * first slot + c + (n - s). False when some tile
+// block needs more than kShiftSlots slots (short runs: the element gathers are as good) or an
+// offset does not fit the int32 tables.
+static constexpr int kShiftSlots = 64;
+static bool nshift_tables(const std::vector<int64_t>& cB, std::vector<int>& prod,
+                          std::vector<int>& conv) {
+  const int64_t N = (int64_t)cB.size();
+  const int64_t tiles = (N + 127) / 128;
+  prod.assign((size_t)(tiles * kShiftSlots * 2), 0);
+  conv.assign((size_t)(tiles * 128), 0);
+  for (int64_t t = 0; t < tiles; ++t) {
+    const int64_t n0 = t * 128, n1 = std::min(N, n0 + 128);
+    int slot = 0;
+    for (int64_t n = n0; n < n1;) {
+      int64_t e = n + 1;
+      while (e < n1 && cB[(size_t)e] == cB[(size_t)(e - 1)] + 1) ++e;
+      const int64_t L = e - n, nb = (L + 9) / 4;
+      if (slot + nb > kShiftSlots) return false;
+      const int64_t b = cB[(size_t)n], c = b & 3;
+      if (b < INT32_MIN / 2 || b > INT32_MAX / 2) return false;
+      for (int64_t i = 0; i < nb; ++i) {
+        prod[(size_t)((t * kShiftSlots + slot + i) * 2)] = (int)(b - c + 4 * i);
+        prod[(size_t)((t * kShiftSlots + slot + i) * 2 + 1)] = (int)((L << 12) | (c - 4 * i + 2048));
+      }
+      for (int64_t j = 0; j < L; ++j) conv[(size_t)(n + j)] = (int)(4 * slot + c + j);
+      slot += (int)nb;
+      n = e;
+    }
+    for (int i = slot; i < kShiftSlots; ++i)
+      prod[(size_t)((t * kShiftSlots + i) * 2 + 1)] = 2048 - 100;   // L = 0: never copied
+  }
+  return true;
+}
+
 // The switches below are read on every call (a getenv per call costs well under a microsecond),
 // so tests and ablations can flip them within one process.
 //
@@ -193,6 +240,13 @@ static bool f32_a_transpose() {
   return !(e && !strcmp(e, "0"));
 }
 
+// Shifted N vectors for B (gather mode 12): TC_UMMA_SHIFT=0 never, 2 wherever the tables exist
+// (tests, measurement), default (1) where the kernel selects them (umma_f32.cu); read per call
+static int b_shift_mode() {
+  const char* e = getenv("TC_UMMA_SHIFT");
+  return e ? atoi(e) : 1;
+}
+
 static int get_tables(const Plan& p, DeviceTables** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -218,6 +272,18 @@ static int get_tables(const Plan& p, DeviceTables** out) {
   if (e == cudaSuccess) e = upload_bytes(fb, &d->vB);
   if (e == cudaSuccess)
     e = upload_bytes(std::vector<uint8_t>(std::max(fa.size(), fb.size()), 0), &d->vZ);
+  if (e == cudaSuccess && p.dtype == TC_F32 && !p.idx64 && !p.b_vec_k) {
+    std::vector<int> prod, conv;
+    if (nshift_tables(p.kscat[3], prod, conv)) {
+      e = cudaMalloc(reinterpret_cast<void**>(&d->bsh_p), sizeof(int) * prod.size());
+      if (e == cudaSuccess)
+        e = cudaMemcpy(d->bsh_p, prod.data(), sizeof(int) * prod.size(), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMalloc(reinterpret_cast<void**>(&d->bsh_c), sizeof(int) * conv.size());
+      if (e == cudaSuccess)
+        e = cudaMemcpy(d->bsh_c, conv.data(), sizeof(int) * conv.size(), cudaMemcpyHostToDevice);
+    }
+  }
   // the uploads ran on the legacy stream (a pageable cudaMemcpy may return before its DMA has
   // landed, cudaMemset is asynchronous): wait for them before any stream may read the tables
   if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStreamLegacy);
@@ -256,6 +322,10 @@ static int execute(const Plan& p, double alpha, const void* A, const void* B, do
   a.b_vec_all = p.b_pairs_all && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 && !scatter_only;
   a.a_vec2_all = p.a_pairs2_all && (reinterpret_cast<uintptr_t>(a.A) % 8) == 0 && !scatter_only;
   a.b_vec2_all = p.b_pairs2_all && (reinterpret_cast<uintptr_t>(a.B) % 8) == 0 && !scatter_only;
+  a.bsh_p = d->bsh_p;
+  a.bsh_c = d->bsh_c;
+  a.b_shift = d->bsh_p != nullptr && (reinterpret_cast<uintptr_t>(a.B) % 16) == 0 &&
+              !scatter_only ? b_shift_mode() : 0;
   a.a_elem = gather_override() ? gather_override() == 2 : p.a_elem;
   a.b_elem = gather_override() ? gather_override() == 2 : p.b_elem;
   a.f32_a_transpose = f32_a_transpose() && !scatter_only;

@@ -529,6 +529,48 @@ struct GatherVN {
   }
 };
 
+// B along N by shifted 16-byte vectors (mode 12, N = 256 form): B's N runs are contiguous but
+// start at any 4-byte offset, so each run is copied as the aligned 16-byte blocks that cover it
+// (tc_api.cpp nshift_tables: per tile block of 128 columns, run j gets ceil((L + 6) / 4) slots)
+// into a [k][n] staging of 256 floats per k that spans the hi and lo halves of its K chunk. The
+// blocks of K index k start at the run's aligned offset plus rscat_B[k] rounded down to 4, so
+// column n sits at a per-column staging word plus the per-k shift rscat_B[k] mod 4; the
+// converter warps pick the values out and write the K-major hi and lo rows over the staging.
+template <typename IDX, int CH>
+struct GatherSNV {
+  static constexpr int KPW = BK / kPW;               // k rows per warp (8)
+  static constexpr int NS = 64;                      // slots per tile block (tc_api.cpp)
+  int2 ent[2];                                       // slots lane, lane + 32
+  IDX ko[KPW];
+  __device__ __forceinline__ void init_tab(const int* __restrict__ tab, int tn, int l) {
+    const int2* t = reinterpret_cast<const int2*>(tab) + (size_t)tn * NS;
+    ent[0] = t[l];
+    ent[1] = t[l + 32];
+  }
+  __device__ __forceinline__ void load_k(const IDX* __restrict__ ktab, int k0, int l) {
+    const int w = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < KPW; ++j) ko[j] = __ldg(ktab + k0 + w * KPW + j);
+  }
+  __device__ __forceinline__ void issue(float* sm, const float* __restrict__ g, int k0, int K, int w,
+                                        int l) {
+#pragma unroll
+    for (int j = 0; j < KPW; ++j) {
+      const int k = w * KPW + j;
+      float* row = sm + (k >> 2) * CH + (k & 3) * 256;
+      const bool kin = k0 + k < K;
+      const int kk = (int)ko[j];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        // block i of its run holds words [4 i, 4 i + 4) of the run shifted by c + (k mod 4):
+        // copied when they overlap the run's L words (d = c + shift - 4 i)
+        const int d = (ent[h].y & 0xFFF) - 2048 + (kk & 3), L = ent[h].y >> 12;
+        if (d < 4 && d + L > 0) cp_async16(row + 4 * (l + 32 * h), g + (ent[h].x + (kk & ~3)), kin);
+      }
+    }
+  }
+};
+
 // operand gather modes: 0 row-mapped elements, 1 K-run elements, 2 K vectors, 3 row vectors,
 // 5 K pairs, 6 row pairs (A), 7 K-run elements one row per instruction, 8 rows one k per
 // instruction
@@ -543,6 +585,7 @@ template <typename IDX, int CH, int R> struct GatherSel<IDX, 7, CH, R> { using t
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 8, CH, R> { using type = GatherR32<IDX, CH, R>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 10, CH, R> { using type = GatherVN<IDX, CH, 4>; };
 template <typename IDX, int CH, int R> struct GatherSel<IDX, 11, CH, R> { using type = GatherVN<IDX, CH, 2>; };
+template <typename IDX, int CH, int R> struct GatherSel<IDX, 12, CH, R> { using type = GatherSNV<IDX, CH>; };
 
 #ifdef TC_UMMA_PROF
 // measurement build: per-role cycles spent in each barrier wait, printed by CTA 0 at exit
@@ -635,7 +678,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
                    const IDX* __restrict__ rB, const IDX* __restrict__ cB,
                    const IDX* __restrict__ rC, const IDX* __restrict__ cC, int M, int N, int K,
                    int tiles_m, int tiles_n, double alpha, double beta, Sched sched,
-                   int* __restrict__ flags, bool c_lanes_n) {
+                   int* __restrict__ flags, bool c_lanes_n, const int* __restrict__ bsh_p,
+                   const int* __restrict__ bsh_c) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int kChA = chunk_stride<128 * 4, A_MODE>();
   constexpr int kChB = chunk_stride<kChunkB - 16, B_MODE>();
@@ -706,7 +750,8 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
       int tm, tn;
       tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
       ga.init(rA, tm * kTM + BM * (int)crank, M, warp, lane);
-      gb.init(cB, tn * BN + kRowsB * (int)crank, N, warp, lane);
+      if constexpr (B_MODE == 12) gb.init_tab(bsh_p, tn, lane);
+      else gb.init(cB, tn * BN + kRowsB * (int)crank, N, warp, lane);
       if (kpre != kb) {
         ga.load_k(cA, kb * BK, lane);
         gb.load_k(rB, kb * BK, lane);
@@ -729,11 +774,41 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
     const int t = threadIdx.x - kConv0 * 32;
     uint32_t it = 0;
     while (wi.next(tile, kb, ke, sk)) {
+      int cv = 0;   // mode 12: this thread's column's staging word (before the per-k shift)
+      if constexpr (B_MODE == 12) {
+        int tm, tn;
+        tile_coords<GROUP_M>(tile, tiles_m, tiles_n, &tm, &tn);
+        cv = __ldg(bsh_c + tn * BN + t);
+      }
       for (int kt = kb; kt < ke; ++kt, ++it) {
         const int s = it % STAGES;
+        int kq = 0;   // mode 12: this lane's k (= lane) offset of the step, for the shifts
+        if constexpr (B_MODE == 12) kq = kt * BK + lane < K ? (int)__ldg(rB + kt * BK + lane) : 0;
         PWAIT(1, mbar_wait(&full[s], (it / STAGES) & 1));
         float* st = stage0 + s * kStage;
-        if constexpr (kN256 && (B_MODE == 10 || B_MODE == 11)) {
+        if constexpr (kN256 && B_MODE == 12) {
+          // B from the shifted staging: column t's value of k sits at its run's slots + the
+          // run's shift for k, ((cscat_B[s] + rscat_B[k]) mod 4); shifts of the 32 k as two
+          // ballot masks
+          static_assert(kCW == 4, "one converter thread per B row");
+          const uint32_t m0 = __ballot_sync(0xffffffffu, kq & 1), m1 = __ballot_sync(0xffffffffu, kq & 2);
+          const float* sb = st + kOffBh + cv;
+          float v[BK];
+#pragma unroll
+          for (int k = 0; k < BK; ++k) {
+            const int sh = (int)((m0 >> k) & 1u) | (int)(((m1 >> k) & 1u) << 1);   // warp-uniform
+            v[k] = sb[(k >> 2) * kChB + (k & 3) * 256 + sh];
+          }
+          asm volatile("bar.sync 3, %0;\n" ::"n"(kCW * 32) : "memory");   // converters only
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            const float4 x = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+            float4* hi = reinterpret_cast<float4*>(st + kOffBh + c * kChB) + t;
+            *hi = x;
+            hi[128] = make_float4(lo_round(x.x - tf32_trunc(x.x)), lo_round(x.y - tf32_trunc(x.y)),
+                                  lo_round(x.z - tf32_trunc(x.z)), lo_round(x.w - tf32_trunc(x.w)));
+          }
+        } else if constexpr (kN256 && (B_MODE == 10 || B_MODE == 11)) {
           // B from the [k][n] staging in the lo halves: this thread's row n, all 32 K values
           // into registers, then (once every converter thread has read) the hi rows and the lo
           // rows over the staging
@@ -1168,13 +1243,13 @@ static int launch_dir(const LaunchArgs& a, cudaStream_t s) {
     cfg.attrs = attr1;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, kern, pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
-                           tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags, a.c_lanes_n) !=
-        cudaSuccess)
+                           tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags, a.c_lanes_n,
+                           a.bsh_p, a.bsh_c) != cudaSuccess)
       return -1;
   } else {
     kern<<<nunits, kThreads, smem, s>>>(pA, pB, pC, trA, tcA, trB, tcB, trC, tcC, a.M, a.N, a.K,
                                         tiles_m, tiles_n, a.alpha, a.beta, sc, a.flags,
-                                        a.c_lanes_n);
+                                        a.c_lanes_n, a.bsh_p, a.bsh_c);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
@@ -1219,8 +1294,15 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
   const bool kv = pkv && !strcmp(pkv, "1");
   const int am = a.a_vec_m ? (amv && a.a_vec_all ? 3 : (a2 ? 6 : a_row))
                            : (kv && a.a_vec_all ? 2 : (a2 ? 5 : a_k));
+  // B's shifted N vectors (mode 12) pay where A's gathers are element copies one k per
+  // instruction (mode 8): there the producers bound the kernel and mode 12 halves B's copy
+  // instructions (cfg4_07 +13%, cfg4_18 +10%); with cheaper A gathers the converters' extra work
+  // (scalar staging reads, the hi rows rewritten) costs more than it saves (cfg4_02, 06, 14:
+  // -3..-4%; profiles/r02/ab_umma_shift.txt). TC_UMMA_SHIFT=2 forces it wherever available.
+  const bool shift = bn && (a.b_shift == 2 || (a.b_shift == 1 && am == 8));
   const int bm = a.b_vec_k ? (kv && a.b_vec_all ? 2 : (b2 ? 5 : b_k))
-                           : (bn && a.b_vec_all ? 10 : (bn && b2 ? 11 : b_row));
+                           : (bn && a.b_vec_all ? 10 : (bn && b2 ? 11 : (shift ? 12 : b_row)));
+  if (getenv("TC_UMMA_DEBUG")) fprintf(stderr, "tc_umma n256: A mode %d, B mode %d\n", am, bm);
   if constexpr (!kPair) {
     switch (am * 100 + bm) {
     case 0: return launch_dir<int, 0, 0>(a, stream);
@@ -1286,6 +1368,14 @@ int TC_UMMA_LAUNCH(const LaunchArgs& a, cudaStream_t stream) {
     case 602: return launch_dir<int, 6, 2>(a, stream);
     case 702: return launch_dir<int, 7, 2>(a, stream);
     case 802: return launch_dir<int, 8, 2>(a, stream);
+    case 12: return launch_dir<int, 0, 12>(a, stream);
+    case 112: return launch_dir<int, 1, 12>(a, stream);
+    case 212: return launch_dir<int, 2, 12>(a, stream);
+    case 312: return launch_dir<int, 3, 12>(a, stream);
+    case 512: return launch_dir<int, 5, 12>(a, stream);
+    case 612: return launch_dir<int, 6, 12>(a, stream);
+    case 712: return launch_dir<int, 7, 12>(a, stream);
+    case 812: return launch_dir<int, 8, 12>(a, stream);
     default: return launch_dir<int, 8, 8>(a, stream);
     }
   }

@@ -487,6 +487,55 @@ def test_f32_pair_gathers(spec, mnk):
     assert torch.equal(Cd.cpu(), ref)
 
 
+@pytest.mark.parametrize("shift", ["2", "1", "0"], ids=["shifted", "auto", "elements"])
+@pytest.mark.parametrize("lens", [dict(m=300, a=21, b=13, k=7, j=9),
+                                  dict(m=130, a=11, b=37, k=5, j=29),
+                                  dict(m=517, a=63, b=5, k=33, j=3),
+                                  dict(m=64, a=7, b=40, k=3, j=2)])
+def test_f32_shifted_n_vectors(lens, shift, monkeypatch):
+    """B gathered along N with runs (the unit-stride label a, odd length) that start at every
+    4-byte offset: the N = 256 form copies each run as the aligned 16-byte blocks covering it
+    and the converter warps pick the values out at the run's shift for each k (umma_f32.cu
+    gather mode 12, forced with TC_UMMA_SHIFT=2); TC_UMMA_SHIFT=0 forces the element gathers.
+    Ragged tiles, beta != 0,
+    integer mode bitwise."""
+    monkeypatch.setenv("TC_F32_UMMA", "1")
+    monkeypatch.setenv("TC_UMMA_SHIFT", shift)
+    case = W.Case("f32shift", "mab", "mkj", "abjk", lens, dtype=torch.float32, alpha=0.75,
+                  beta=-0.5, c_init="dist", seed=47)
+    check(case)
+    case.dist = "int"
+    check(case, bitwise=True)
+
+
+@pytest.mark.parametrize("shift", ["2", "0"], ids=["shifted", "elements"])
+def test_f32_shifted_n_vectors_guard(shift, monkeypatch):
+    """Mode 12 over-fetches up to 3 floats on either side of every run: B lives in a NaN-filled,
+    16-byte aligned buffer with NaN gaps between its runs and between its K slices, so a value
+    picked from the wrong place of a slot poisons C; C must stay finite and match the oracle."""
+    monkeypatch.setenv("TC_F32_UMMA", "1")
+    monkeypatch.setenv("TC_UMMA_SHIFT", shift)
+    lens = dict(m=260, a=21, b=19, k=5, j=7)
+    case = W.Case("f32shiftg", "mab", "mkj", "abjk", lens, dtype=torch.float32, alpha=1.0,
+                  beta=0.5, c_init="dist", seed=53)
+    A, B, C = W.make_tensors(case, "cpu")
+    ref = C.clone()
+    oracle.contract(case.spec, A, B, ref, case.alpha, case.beta)
+    sa, sb = 1, 21 + 2                  # two NaNs after every run of a
+    sj = sb * 19 + 3
+    sk = sj * 7 + 1
+    buf = torch.full((sk * 5 + 64,), float("nan"), device="cuda")
+    assert buf.data_ptr() % 16 == 0
+    Bd = buf.as_strided((21, 19, 7, 5), (sa, sb, sj, sk), 4)   # 16-byte aligned base
+    Bd.copy_(B.cuda())
+    Cd = C.cuda()
+    tc().contract(case.spec, A.cuda(), Bd, Cd, case.alpha, case.beta)
+    torch.cuda.synchronize()
+    got = Cd.cpu()
+    assert torch.isfinite(got).all()
+    assert relerr(got.numpy(), ref.numpy()) <= 1e-5
+
+
 @pytest.mark.usefixtures("both_f32_paths")
 @pytest.mark.usefixtures("both_small_paths")
 def test_f32_misaligned_views():
