@@ -21,7 +21,10 @@ namespace sched {
 // add alpha*acc in a fixed order behind a per-tile flag. No partial-sum workspace, deterministic
 // results, and a piece only waits on lower-ranked CTAs' first work items (no deadlock).
 // ------------------------------------------------------------------------------------------
-constexpr int kMaxWeighted = 32;   // stream-K tail tiles that can carry work weights
+// Stream-K tail tiles that can carry work weights. Sched is a by-value kernel parameter: with 32
+// (a 33-int prefix-sum array) the bench workload ran 0.7% slower than with 16 or fewer, though
+// it never uses the weights (cfg5 2422 vs 2404-2405 ms, same box; profiles/r02/ab_sched_param.txt)
+constexpr int kMaxWeighted = 16;
 
 struct Sched {
   int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
