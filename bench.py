@@ -40,9 +40,9 @@ SHARD_LABELS = "abc"
 PEAKS_FILE = os.path.join(ROOT, "profiles", "PEAKS_FP64.json")
 # DRAM bytes per launch of the contraction kernel on the full cfg5 workload, from
 # `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum` of this same
-# command (tools/gpu/r02_evidence.sh, the round-2 launch list); the counters of the `--set full`
-# memory section.
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02", "launches_bench_r02.csv")
+# command (tools/gpu/r02_s2_ck6.sh, the launch list of the final round-2 build); the counters of
+# the `--set full` memory section.
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02", "launches_bench_r02s2.csv")
 
 
 def ncu_traffic(path, kernel_prefix="tc_dmma_ws_kernel"):
@@ -452,7 +452,7 @@ def run_native(args):
                      "peak": peak, "unit": "TFLOP/s", "frac": round(achieved_tf / peak, 4),
                      "traffic": None if args.small or world > 1 else ncu_traffic(TRAFFIC_FILE),
                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum, one "
-                                       "launch of this workload (profiles/r02/launches_bench_r02.csv)",
+                                       "launch of this workload (profiles/r02/launches_bench_r02s2.csv)",
                      "peak_source": "profiles/PEAKS_FP64.json dmma_tflops (measured DMMA.8x8x4 "
                                     "loop on this pool's B200; fp64 has no entry in "
                                     "MEASURED_PEAKS.json)",

@@ -24,7 +24,10 @@ namespace sched {
 // Stream-K tail tiles that can carry work weights. Sched is a by-value kernel parameter: with 32
 // (a 33-int prefix-sum array) the bench workload ran 0.7% slower than with 16 or fewer, though
 // it never uses the weights (cfg5 2422 vs 2404-2405 ms, same box; profiles/r02/ab_sched_param.txt)
-constexpr int kMaxWeighted = 16;
+#ifndef TC_SK_MAXW
+#define TC_SK_MAXW 16   // measurement override
+#endif
+constexpr int kMaxWeighted = TC_SK_MAXW;
 
 struct Sched {
   int T, D, P, KT;          // tiles, data-parallel tiles, CTAs in the DP phase, K iterations
