@@ -1265,9 +1265,13 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   if (!ensure_dyn_smem(kern, smem, attr)) return -1;
   const int tiles_m = (a.M + BM - 1) / BM, tiles_n = (a.N + BN - 1) / BN;
   const int KT = (a.K + BK - 1) / BK;
-  static const int dp_pct = [] {   // measurement override of the 88% threshold (TC_WS_DPPCT)
+  // every partial wave goes to the stream-K tail (threshold 101%): since the fix-ups add at L2
+  // (red.global.add) a split tail beats a nearly full data-parallel wave (cfg4_11 fp64 +3.8%,
+  // cfg4_12 +1.2%, geomean over cfg4 fp64 / f1 / f2 +0.07%; round 1's 88% was measured with
+  // load-add-store fix-ups; profiles/r02/ab_dppct.txt). TC_WS_DPPCT overrides (measurement).
+  static const int dp_pct = [] {
     const char* e = getenv("TC_WS_DPPCT");
-    return e ? atoi(e) : 88;
+    return e ? atoi(e) : 101;
   }();
   // up to 48 stream-K pieces per tile: few-tile, long-K shapes then keep every SM busy (this
   // kernel's fix-up links are cheap: 256^2 x 65536 0.39 -> 0.52, 128^2 x 262144 0.12 -> 0.27 of

@@ -188,7 +188,8 @@ inline Sched make_sched(int T, int KT, int nsm, bool allow_sk, int dp_pct = 88,
   // enough iterations per CTA for a short tail), unless the partial wave is >= 88% full, which
   // then runs data-parallel (its idle share is smaller than the cost of the split pieces'
   // extra epilogues). Measured on cfg4 (profiles/r01/ab_sk_policy.txt); the fp32 tcgen05
-  // kernel passes dp_pct = 70 (profiles/r01/ab_umma_sk.txt).
+  // kernel passes dp_pct = 70 (profiles/r01/ab_umma_sk.txt), the DMMA kernel 101 since its
+  // fix-ups add at L2 (profiles/r02/ab_dppct.txt).
   int D;
   const int rem = T % nsm;
   if (!allow_sk || KT == 0 || rem == 0 || rem * 100 >= dp_pct * nsm) D = T;
