@@ -166,8 +166,20 @@ __global__ void __launch_bounds__(kThreads, MAXK <= 8 ? TC_RANKK_MINB : 4) tc_ra
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nblocks = (N + kNB - 1) / kNB;
   // this CTA's column blocks: blockIdx.y + i gridDim.y, i < nu
+  // each CTA walks a consecutive range of column blocks: the CTAs resident together (all row
+  // blocks of a few grid rows) then write few, long stretches of C, which HBM takes faster than
+  // the interleaved stretches of a strided walk (f1 k = 5: 4.89 -> 5.16 TB/s;
+  // profiles/r02/ab_rankk_walk.txt; tools/calib/write_pattern.cu). TC_RANKK_STRIDED (build
+  // flag): the strided walk y, y + gy, ... of round 2's first version.
+#ifdef TC_RANKK_STRIDED
   const int nu = blockIdx.y < nblocks ? (nblocks - 1 - (int)blockIdx.y) / (int)gridDim.y + 1 : 0;
   auto cb_of = [&](int i) { return (int)blockIdx.y + i * (int)gridDim.y; };
+#else
+  const int per = (nblocks + (int)gridDim.y - 1) / (int)gridDim.y;
+  const int cb0 = (int)blockIdx.y * per;
+  const int nu = cb0 < nblocks ? min(per, nblocks - cb0) : 0;
+  auto cb_of = [&](int i) { return cb0 + i; };
+#endif
   // the K offsets of Y, once
   IDX ky[MAXK];
 #pragma unroll
