@@ -337,6 +337,18 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
   __syncthreads();
 
   const int nblk = (a.R + kRows - 1) / kRows;
+  // The CTA's blocks: blockIdx.x, + gridDim.x, ... (the CTAs running together stream one
+  // moving window of X and C), or a consecutive range per CTA (TC_SKINNY_CONSEC build flag,
+  // measurement: 0.85-0.95x on the HBM-bound strings, though it helps the rank-k kernel's
+  // write-only stream; profiles/r02/ab_skinny_walk.txt)
+#ifndef TC_SKINNY_CONSEC
+  auto blk_of = [&](int i) { return (int)blockIdx.x + i * (int)gridDim.x; };
+  const int nloc = (int)blockIdx.x < nblk ? (nblk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+#else
+  const int per = (nblk + (int)gridDim.x - 1) / (int)gridDim.x;
+  auto blk_of = [&](int i) { return (int)blockIdx.x * per + i; };
+  const int nloc = max(0, min(per, nblk - (int)blockIdx.x * per));
+#endif
   if (warp < kWsProd) {
     // ---- producers: rows-unit lanes take rows 32 h + lane (sub-divided as in the synchronous
     // kernel) for K rows warp, warp + 4, ..; K-unit lanes take 8 consecutive K entries of rows
@@ -369,13 +381,12 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
       }
     };
 #pragma unroll
-    for (int d = 0; d < kWsAhead; ++d) rows(blockIdx.x + d * gridDim.x, ro[d], rv[d]);
-    for (int i0 = 0; blockIdx.x + i0 * gridDim.x < nblk; i0 += kWsAhead) {
+    for (int d = 0; d < kWsAhead; ++d) rows(d < nloc ? blk_of(d) : nblk, ro[d], rv[d]);
+    for (int i0 = 0; i0 < nloc; i0 += kWsAhead) {
 #pragma unroll
       for (int d = 0; d < kWsAhead; ++d) {
         const int i = i0 + d;
-        const int blk = blockIdx.x + i * gridDim.x;
-        if (blk >= nblk) break;
+        if (i >= nloc) break;
         const int q = i % S;
         if (i >= S) mbar_wait(&empty[q], ((i / S) - 1) & 1);
         double* dst = xs + q * stage;
@@ -402,7 +413,7 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
           }
         }
         mbar_cp_async_arrive(&full[q]);
-        rows(blockIdx.x + (i + kWsAhead) * gridDim.x, ro[d], rv[d]);
+        rows(i + kWsAhead < nloc ? blk_of(i + kWsAhead) : nblk, ro[d], rv[d]);
       }
     }
     cp_async_wait_all();
@@ -435,14 +446,14 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
 #pragma unroll
     for (int h = 0; h < 2; ++h) o[h] = (blk < nblk && r0 + 8 * h < a.R) ? cr[r0 + 8 * h] : 0;
   };
-  crows(blockIdx.x + grp * gridDim.x, cro[0]);
-  crows(blockIdx.x + (grp + CG) * gridDim.x, cro[1]);
-  for (int i0 = grp; blockIdx.x + i0 * gridDim.x < nblk; i0 += 2 * CG) {
+  crows(grp < nloc ? blk_of(grp) : nblk, cro[0]);
+  crows(grp + CG < nloc ? blk_of(grp + CG) : nblk, cro[1]);
+  for (int i0 = grp; i0 < nloc; i0 += 2 * CG) {
 #pragma unroll
   for (int d = 0; d < 2; ++d) {
     const int i = i0 + d * CG;
-    const int blk = blockIdx.x + i * gridDim.x;
-    if (blk >= nblk) break;
+    if (i >= nloc) break;
+    const int blk = blk_of(i);
     const int q = i % S;
     mbar_wait(&full[q], (i / S) & 1);
     const double* xb = xs + q * stage;
@@ -494,7 +505,7 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
           }
       }
     }
-    crows(blockIdx.x + (i + 2 * CG) * gridDim.x, cro[d]);
+    crows(i + 2 * CG < nloc ? blk_of(i + 2 * CG) : nblk, cro[d]);
   }
   }
 }
