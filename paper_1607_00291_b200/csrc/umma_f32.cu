@@ -621,6 +621,28 @@ __device__ __noinline__ void rmw_block_transposed(const float* stg, float* C, ID
   }
 }
 
+// Stream-K fix-up of a later piece (piece > 0): the block's alpha * acc is added into C at L2
+// with red.global.add.f32, no read of C (the flags still fix the order of the pieces, and the
+// piece's fence before publishing waits for the reductions), through the same transpose.
+// TC_UMMA_RED=0 (build flag): load-add-store instead (rmw_block_transposed).
+#ifndef TC_UMMA_RED
+#define TC_UMMA_RED 1
+#endif
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+template <typename IDX>
+__device__ __noinline__ void red_block_transposed(const float* stg, float* C, IDX rc, IDX col,
+                                                  int mrow0, int M, bool cin, double alpha,
+                                                  int lane) {
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const IDX rr = __shfl_sync(0xffffffffu, rc, r);
+    if (cin && mrow0 + r < M)
+      red_add_f32(C + (rr + col), static_cast<float>(alpha * static_cast<double>(stg[r * 33 + lane])));
+  }
+}
+
 // Write-only counterpart (TC_UMMA_WT=1: measurement switch): alpha * block through the same
 // transpose, one 128-byte row segment per warp store.
 #ifndef TC_UMMA_WT
@@ -1023,8 +1045,11 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
 #pragma unroll
               for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = __uint_as_float(u[i]);
               __syncwarp();
-              rmw_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, piece, alpha,
-                                        beta, lane);
+              if (TC_UMMA_RED && piece > 0)
+                red_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, alpha, lane);
+              else
+                rmw_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, piece,
+                                          alpha, beta, lane);
               __syncwarp();
             } else if (TC_UMMA_WT && !read_c && c_lanes_n) {
               float* stg = epi_stage + q * 32 * 33;
@@ -1033,6 +1058,14 @@ tc_umma_f32_kernel(const float* __restrict__ A, const float* __restrict__ B, flo
               __syncwarp();
               store_block_transposed<IDX>(stg, C, rc, col, m - lane, M, nb + lane < N, alpha, lane);
               __syncwarp();
+            } else if (TC_UMMA_RED && piece > 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const IDX o = __shfl_sync(0xffffffffu, col, i);
+                if (min_ && (full || nb + i < N))
+                  red_add_f32(C + (rc + o),
+                              static_cast<float>(alpha * static_cast<double>(__uint_as_float(u[i]))));
+              }
             } else if (read_c) {
               float old[32];
 #pragma unroll
