@@ -299,6 +299,23 @@ constexpr int kWsProd = 4;
 constexpr int kWsMaxK4 = 8;   // KP <= 32
 constexpr int kWsAhead = 4;   // producer: row-offset lookahead (blocks)
 
+// X copies of the warp-specialised producers: 8-byte cp.async, optionally with an L2 prefetch
+// hint (TC_SKINNY_L2HINT = 128 | 256 build flag, measurement; profiles/r02/ab_skinny_l2hint.txt)
+#ifndef TC_SKINNY_L2HINT
+#define TC_SKINNY_L2HINT 0
+#endif
+__device__ __forceinline__ void cp_async8_x(void* smem, const void* gmem, bool pred) {
+  const int sz = pred ? 8 : 0;
+  if constexpr (TC_SKINNY_L2HINT == 256)
+    asm volatile("cp.async.ca.shared.global.L2::256B [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+                 "l"(gmem), "r"(sz));
+  else if constexpr (TC_SKINNY_L2HINT == 128)
+    asm volatile("cp.async.ca.shared.global.L2::128B [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)),
+                 "l"(gmem), "r"(sz));
+  else
+    cp_async8(smem, gmem, pred);
+}
+
 // YREG: Y's fragments live in registers (NP, KP <= 32); otherwise the consumers read them from
 // shared memory per block (block_mma), for the larger resident operands (K, N <= 80, 96).
 template <typename IDX, bool ROWS_UNIT, int NW, int CG, bool YREG>
@@ -398,7 +415,7 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
             const IDX ko = xks[k];
 #pragma unroll
             for (int h = 0; h < H; ++h)
-              cp_async8(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), kin && rv[d][h]);
+              cp_async8_x(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), kin && rv[d][h]);
           }
         } else {
           const int kk = lane & 7;
@@ -408,7 +425,7 @@ __global__ void __launch_bounds__(32 * (kWsProd + 8 * CG), 1) tc_skinny_ws_kerne
               const IDX ko = xks[k];
 #pragma unroll
               for (int h = 0; h < H; ++h)
-                cp_async8(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), rv[d][h] && k < a.K);
+                cp_async8_x(dst + k * xp + pl[h], a.X + (ro[d][h] + ko), rv[d][h] && k < a.K);
             }
           }
         }
