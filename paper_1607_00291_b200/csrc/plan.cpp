@@ -380,13 +380,29 @@ Status build_plan(tc_dtype dtype, const tc_tensor& A, const tc_tensor& B, const 
       (p->n <= 96 || p->m <= 96)) {
     std::vector<Dim>& L = p->n <= 96 ? p->kb.I : p->kb.J;   // long bundle; X = A or B
     const int u = find_unit(L, 0), v = find_unit(L, 1);
-    auto divisor = [](int64_t len) {   // a power of two, so bu * bv divides the 64-row block
-      for (int64_t b = 8; b >= 2; b /= 2)
+    auto divisor = [](int64_t len, int64_t cap) {   // a power of two, so bu * bv divides the
+      for (int64_t b = cap; b >= 2; b /= 2)           // 64-row block
         if (len % b == 0) return b;
       return (int64_t)1;
     };
+    // run-length caps (measurement overrides read per plan): TC_SKINNY_BV = 2..32 for C's runs,
+    // TC_SKINNY_BU = 2..32 for X's; the other then caps at 64 / that one (measured: 8 and 8,
+    // profiles/r02/ab_skinny_runs.txt)
+    auto cap_env = [](const char* name) -> int64_t {
+      const char* e = getenv(name);
+      const int64_t c = e ? atoi(e) : 0;
+      return c == 2 || c == 4 || c == 8 || c == 16 || c == 32 ? c : 0;
+    };
+    const int64_t bv_env = cap_env("TC_SKINNY_BV"), bu_env = cap_env("TC_SKINNY_BU");
     if (u >= 0 && v >= 0 && u != v) {
-      const int64_t bu = divisor(L[(size_t)u].len), bv = divisor(L[(size_t)v].len);
+      int64_t bv, bu;
+      if (bu_env) {
+        bu = divisor(L[(size_t)u].len, bu_env);
+        bv = divisor(L[(size_t)v].len, std::min<int64_t>(bv_env ? bv_env : 8, 64 / bu));
+      } else {
+        bv = divisor(L[(size_t)v].len, bv_env ? bv_env : 8);
+        bu = divisor(L[(size_t)u].len, std::min<int64_t>(8, 64 / bv));
+      }
       if (bu > 1 && bv > 1) {
         const Dim du = L[(size_t)u], dv = L[(size_t)v];
         auto part = [](const Dim& d, int64_t len, int64_t mul, const char* tag) {

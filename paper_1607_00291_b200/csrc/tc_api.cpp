@@ -390,6 +390,8 @@ static int get_plan(tc_dtype dtype, const tc_tensor* A, const tc_tensor* B, cons
     return rc;
   std::string key(1, (char)dtype);
   key_tensor(key, *A); key_tensor(key, *B); key_tensor(key, *C);
+  for (const char* ov : {"TC_SKINNY_BV", "TC_SKINNY_BU"})   // planner overrides (plan.cpp)
+    if (const char* e = getenv(ov)) { key.append(ov); key.append(e); }
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     auto it = g_cache.find(key);

@@ -922,6 +922,23 @@ def test_skinny_ring_skew(lens, sw, monkeypatch):
     check(case, bitwise=True)
 
 
+@pytest.mark.parametrize("lens", [
+    {"a": 32, "b": 5, "c": 32, "d": 7, "e": 32, "f": 32},    # bv = 16 / 32, bu = 4 / 2
+    {"a": 48, "b": 3, "c": 20, "d": 9, "e": 24, "f": 12},    # bv = 16, bu = 4; ragged last block
+])
+@pytest.mark.parametrize("env", ["TC_SKINNY_BV=16", "TC_SKINNY_BV=32", "TC_SKINNY_BU=16",
+                                 "TC_SKINNY_BU=32"])
+def test_skinny_run_lengths(lens, env, monkeypatch):
+    """Other run lengths in the skinny sub-division (TC_SKINNY_BV / _BU: C's or X's runs up to 16
+    or 32 elements, the other's capped at 64 / that): bitwise the oracle's result on integer
+    inputs, alpha and beta != 0."""
+    name, val = env.split("=")
+    monkeypatch.setenv(name, val)   # part of the plan-cache key
+    case = W.Case("skinny_bv", "abcde", "efbad", "cf", lens, alpha=2.0, beta=0.5,
+                  dist="int", c_init="dist", seed=41)
+    check(case, bitwise=True)
+
+
 # ---------------------------------------------------------------------------------------------
 # negative strides (accepted for A, B and C by the C ABI, reading R7) through the raw binding
 # ---------------------------------------------------------------------------------------------
