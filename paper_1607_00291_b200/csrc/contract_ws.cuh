@@ -887,10 +887,12 @@ tc_dmma_ws_kernel(const T* __restrict__ A, const T* __restrict__ B, T* __restric
           for (int c = 0; c < 8; ++c)
             part[mk.col(c) * kPP + mk.row(r)] = static_cast<double>(mk.value(r, c));
         cluster_sync_all();
-        const int S = sched.csplit, RS = BM / S;
+        // rank r sums rows [r BM / S, (r + 1) BM / S) (S need not divide BM)
+        const int S = sched.csplit;
         const uint32_t rank = cluster_rank();
+        const int r0 = (int)rank * BM / S, RS = ((int)rank + 1) * BM / S - r0;
         for (int e = threadIdx.x; e < RS * BN; e += NCW * 32) {
-          const int row = (int)rank * RS + e % RS, col = e / RS;
+          const int row = r0 + e % RS, col = e / RS;
           const uint32_t loc = smem_u32(part + col * kPP + row);
           double v[16];
 #pragma unroll
@@ -1208,10 +1210,11 @@ inline void set_tile_weights(Sched& sc, int M, int N, int tiles_m, int tiles_n) 
 // would use, with >= 2 K steps per CTA. TC_CSK=0 turns it off (read per call).
 template <typename K>
 inline int max_active_clusters(K kern, int S, int smem) {
-  static std::atomic<int> cache[kMaxDevices][5];   // S = 1 << (i + 0): 1, 2, 4, 8, 16
+  static std::atomic<int> cache[kMaxDevices][17];   // by S = 1 .. 16
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
-  const int i = S == 16 ? 4 : S == 8 ? 3 : S == 4 ? 2 : S == 2 ? 1 : 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices || S < 1 || S > 16)
+    return 0;
+  const int i = S;
   int v = cache[dev][i].load(std::memory_order_relaxed);
   if (v > 0) return v - 1;
   cudaLaunchConfig_t cfg = {};
@@ -1248,7 +1251,13 @@ inline int csk_split(const Sched& sc, int nsm, bool allow, Kern kern, int smem) 
     if (!allow || (e && *e == '0') || sc.D != 0 || sc.P_sk < 4 * sc.T) return 0;
     const char* em = getenv("TC_CSK_MAX");
     const int smax = em && atoi(em) == 16 ? 16 : 8;
-    for (int S = smax; S >= 4; S /= 2)
+    // S in {smax, 7, 6, 5, 4}: a cluster size that is not a power of two lets a few-tile shape
+    // whose T clusters of 8 do not fit in one wave still spread its tiles over most SMs (fp64
+    // 512^3: 16 clusters of 8 do not fit, 16 of 7 do; TC_CSK_POW2=1: {smax, 4} only, the
+    // earlier policy; profiles/r02/ab_csk_sizes.txt)
+    const char* ep = getenv("TC_CSK_POW2");
+    const bool pow2 = ep && *ep == '1';
+    for (int S = smax; S >= 4; S = (S == 16 || pow2) ? S / 2 : S - 1)
       if (sc.T * S <= nsm && sc.KT >= 2 * S && 5 * sc.T * S >= 4 * sc.P_sk &&
           sc.T <= max_active_clusters(kern, S, smem))
         return S;

@@ -587,16 +587,19 @@ def test_stream_k_work_weights(mnk, beta, weights, monkeypatch):
     check(case, bitwise=True)
 
 
-@pytest.mark.parametrize("csk", ["0", "8", "16"])
+@pytest.mark.parametrize("csk", ["0", "8", "16", "pow2"])
 @pytest.mark.parametrize("mnk", [(512, 512, 512), (323, 323, 3000), (200, 700, 1000),
-                                 (1024, 1024, 600), (130, 129, 70)])
+                                 (1024, 1024, 600), (130, 129, 70), (640, 640, 640),
+                                 (512, 640, 768), (500, 380, 900)])
 @pytest.mark.parametrize("beta", [0.0, 0.75])
 def test_cluster_split_k(mnk, beta, csk, monkeypatch):
     """Few-tile fp64 shapes through cluster split-K (Sched::csplit: S CTAs of a cluster share a
     tile's K loop, partials summed in rank order through distributed shared memory; S up to 8,
-    or 16 non-portable with TC_CSK_MAX=16) and through the stream-K fix-up chain (TC_CSK=0):
+    or 16 non-portable with TC_CSK_MAX=16; sizes 5-7, whose row shares of the 128-row tile are
+    uneven, unless TC_CSK_POW2=1) and through the stream-K fix-up chain (TC_CSK=0):
     bitwise equal to the oracle on integer inputs, ragged edges, beta != 0, both C layouts."""
     monkeypatch.setenv("TC_CSK", "0" if csk == "0" else "1")
+    monkeypatch.setenv("TC_CSK_POW2", "1" if csk == "pow2" else "0")
     monkeypatch.setenv("TC_CSK_MAX", "16" if csk == "16" else "8")
     m, n, k = mnk
     for spec in ("mn-mk-kn", "nm-km-nk"):
