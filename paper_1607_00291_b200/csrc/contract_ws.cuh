@@ -1203,14 +1203,16 @@ inline void set_tile_weights(Sched& sc, int M, int N, int tiles_m, int tiles_n) 
 }
 
 // Cluster split-K instead of the stream-K schedule (Sched::csplit) where the stream-K split
-// would chain >= 4 pieces per tile (every tile in the tail): the largest S in {8, 4} (16,
-// non-portable, with TC_CSK_MAX=16) whose T clusters are co-resident in one wave (clusters must
-// sit inside a GPC: at 227 KB per CTA only 15 clusters of 8 and 33 of 4 fit on a B200, so 16
-// tiles in clusters of 8 take two waves) and whose T S CTAs cover >= 80% of the SMs stream-K
-// would use, with >= 2 K steps per CTA. TC_CSK=0 turns it off (read per call).
+// would chain >= 4 pieces per tile (every tile in the tail): the largest S in 8 .. 4 (16 .. 4,
+// non-portable, for short pieces) whose T clusters are co-resident in one wave (clusters must
+// sit inside a GPC: at 227 KB per CTA only 15 clusters of 8, 22 of 6 and 33 of 4 fit on a B200,
+// so 16 tiles in clusters of 8 take two waves) and whose T S CTAs cover >= 80% (short pieces:
+// 40%) of the CTAs stream-K would run, with >= 2 K steps per CTA. TC_CSK=0 turns it off (read
+// per call).
 template <typename K>
-inline int max_active_clusters(K kern, int S, int smem) {
-  static std::atomic<int> cache[kMaxDevices][17];   // by S = 1 .. 16
+inline int max_active_clusters(K kern, int S, int smem, std::atomic<int> (*cache)[17]) {
+  // cache: the caller's, one per kernel instantiation (by device and S = 1 .. 16); the
+  // non-portable attribute below is set per kernel as well
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices || S < 1 || S > 16)
     return 0;
@@ -1243,23 +1245,32 @@ inline int max_active_clusters(K kern, int S, int smem) {
 }
 
 template <typename T, bool A_VM, bool B_VK, typename IDX, bool FFMA, typename Kern>
-inline int csk_split(const Sched& sc, int nsm, bool allow, Kern kern, int smem) {
+inline int csk_split(const Sched& sc, int nsm, bool allow, Kern kern, int smem,
+                     std::atomic<int> (*cache)[17]) {
   if constexpr (!csk_fits<T, A_VM, B_VK, IDX, FFMA>()) {
     return 0;
   } else {
     const char* e = getenv("TC_CSK");
     if (!allow || (e && *e == '0') || sc.D != 0 || sc.P_sk < 4 * sc.T) return 0;
+    // Short stream-K pieces (<= 64 K steps per CTA): the chain of fix-ups per tile, not the
+    // arithmetic, sets the time, so cluster split-K pays even on fewer SMs: coverage >= 40% and
+    // non-portable clusters up to 16 (323^2 x 3000 0.34 -> 0.73 of DGEMM, 384^2 x 4096 0.42 ->
+    // 0.69). Long pieces keep >= 80% and S <= 8 (at 40%, f2_16 / f2_17 with K = 104329 fell
+    // 0.77 -> 0.43, 0.89 -> 0.46; profiles/r02/ab_csk_sizes.txt). TC_CSK_COV / _MAX override.
+    const bool short_pieces = (long long)sc.T * sc.KT <= 64LL * sc.P_sk;
     const char* em = getenv("TC_CSK_MAX");
-    const int smax = em && atoi(em) == 16 ? 16 : 8;
+    const int smax = em && atoi(em) >= 4 && atoi(em) <= 16 ? atoi(em) : short_pieces ? 16 : 8;
     // S in {smax, 7, 6, 5, 4}: a cluster size that is not a power of two lets a few-tile shape
     // whose T clusters of 8 do not fit in one wave still spread its tiles over most SMs (fp64
-    // 512^3: 16 clusters of 8 do not fit, 16 of 7 do; TC_CSK_POW2=1: {smax, 4} only, the
+    // 512^3: 16 clusters of 8 or 7 do not fit, 16 of 6 do; TC_CSK_POW2=1: {smax, 4} only, the
     // earlier policy; profiles/r02/ab_csk_sizes.txt)
+    const char* ec = getenv("TC_CSK_COV");
+    const int cov = ec && atoi(ec) > 0 ? atoi(ec) : short_pieces ? 40 : 80;
     const char* ep = getenv("TC_CSK_POW2");
     const bool pow2 = ep && *ep == '1';
-    for (int S = smax; S >= 4; S = (S == 16 || pow2) ? S / 2 : S - 1)
-      if (sc.T * S <= nsm && sc.KT >= 2 * S && 5 * sc.T * S >= 4 * sc.P_sk &&
-          sc.T <= max_active_clusters(kern, S, smem))
+    for (int S = smax; S >= 4; S = pow2 ? (S > 8 ? 8 : S / 2) : S - 1)
+      if (sc.T * S <= nsm && sc.KT >= 2 * S && 100 * sc.T * S >= cov * sc.P_sk &&
+          sc.T <= max_active_clusters(kern, S, smem, cache))
         return S;
     return 0;
   }
@@ -1296,7 +1307,9 @@ int launch(const LaunchArgs& a, cudaStream_t stream) {
   int* flags = a.flags;
   sc.epoch = a.flag_epoch;
   int grid = sc.D > 0 ? sc.P : sc.P_sk;
-  const int S = csk_split<T, A_VM, B_VK, IDX, FFMA>(sc, a.num_sms, a.stream_k, kern, smem);
+  static std::atomic<int> csk_cache[kMaxDevices][17];
+  const int S = csk_split<T, A_VM, B_VK, IDX, FFMA>(sc, a.num_sms, a.stream_k, kern, smem,
+                                                    csk_cache);
   if (S > 0) {
     Sched cs = make_sched(sc.T, KT, a.num_sms, false);
     cs.csplit = S;
